@@ -1,0 +1,422 @@
+"""Benchmark of the octree background-model hot path (BASELINE.json metric).
+
+Workload (BASELINE.json configs[3], the config the metric's 70 %-of-HBM target
+is quoted on): 1920x1080 RGB, octree depth L=6, one step = build the model
+from N=64 training frames (per-frame presence trees + frequency merge) and
+classify 256 test frames in one launch, on synthetic seeded frames
+(paper_1412_1945_b200.scenes; the paper's datasets are not available).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  Under torchrun each rank processes its own
+shard (weak scaling); the model is trained from all ranks' training frames
+with one NCCL all-reduce of per-node tree counts.
+"""
+
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "classify+build Mpixels/s on 1 B200 and % of HBM roofline; bit-exact vs CPU oracle"
+CONFIG_ID = 3
+L2_BYTES = 126 * 2 ** 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--seed", type=int, default=1412)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def golden_record():
+    try:
+        with open(os.path.join(REPO, "tests", "golden", "golden.json")) as f:
+            g = json.load(f)
+        return next(r for r in g["configs"] if r["config"] == CONFIG_ID)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU reference / oracle timing
+# ---------------------------------------------------------------------------
+def _reference_module():
+    """The unmodified reference (installed into baseline/_ref), or None."""
+    path = os.path.join(REPO, "baseline", "_ref")
+    if os.path.isdir(os.path.join(path, "octabg")):
+        sys.path.insert(0, path)
+        try:
+            import octabg
+            return octabg
+        except Exception:
+            return None
+    return None
+
+
+_POOL_STATE = {}
+
+
+def _pool_build(i):
+    ref, train, cfg = _POOL_STATE["ref"], _POOL_STATE["train"], _POOL_STATE["cfg"]
+    return ref.build_frame_tree([train[i]], (0, 0), cfg).to_bytes()
+
+
+def _pool_detect(i):
+    ref, test, model = _POOL_STATE["ref"], _POOL_STATE["test"], _POOL_STATE["model"]
+    return np.packbits(ref.detect_octree(model, test[i]))
+
+
+def cpu_reference_step(ref, train, test, cfg_kw, pool=None):
+    """One bounded sample of the workload through the reference's public API:
+    build_background_model over ``train`` + detect_octree per ``test`` frame.
+    With a fork pool, per-frame trees / masks are computed in workers (trees
+    return via to_bytes), decode + merge stay serial (reference semantics)."""
+    if ref is not None:
+        cfg = ref.ModelConfig(**cfg_kw)
+        if pool is None:
+            model = ref.build_background_model(list(train), cfg)
+            for f in test:
+                ref.detect_octree(model, f)
+            return
+        _POOL_STATE.update(ref=ref, train=train, test=test, cfg=cfg)
+        blobs = pool.map(_pool_build, range(len(train)))
+        trees = [ref.Octree.from_bytes(b, cfg.levels) for b in blobs]
+        merged = ref.merge_trees(trees, cfg.threshold, cfg.levels)
+        model = ref.BackgroundModel(cfg, train.shape[2], train.shape[1], [[merged]])
+        _POOL_STATE["model"] = model
+        pool.map(_pool_detect, range(len(test)))
+        return
+    from oracle import octree_oracle as orc   # port of the reference (no reference install present)
+    model = orc.build_background_model(list(train), cfg_kw["levels"], cfg_kw["threshold"])
+    for f in test:
+        orc.detect_octree(model, f, cfg_kw["levels"])
+
+
+def cpu_baseline(scene, cfg_kw):
+    """Single-process reference on a bounded sample (all 64 training frames +
+    16 test frames), median of 2, on this box's host."""
+    ref = _reference_module()
+    train, test = scene.train, scene.test[:16]
+    times = []
+    for _ in range(2):
+        t0 = time.perf_counter()
+        cpu_reference_step(ref, train, test, cfg_kw)
+        times.append(time.perf_counter() - t0)
+    px = (len(train) + len(test)) * scene.width * scene.height
+    return {"value": round(px / statistics.median(times) / 1e6, 3), "unit": "Mpx/s", "cores": 1,
+            "kind": "reference" if ref is not None else "port",
+            "sample": f"build_background_model on 64 training + detect_octree on 16 test frames of the "
+                      f"1920x1080 L6 scene, single process, median of 2 ({statistics.median(times):.1f} s)"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from multiprocessing import get_context
+    from paper_1412_1945_b200 import scenes
+    n_test = 64
+    scene = scenes.generate(CONFIG_ID, seed=args.seed, n_test=n_test)
+    cfg_kw = dict(levels=scene.config.levels, threshold=scene.config.threshold,
+                  training_frames=len(scene.train))
+    ref = _reference_module()
+    cores = os.cpu_count() or 1
+    _POOL_STATE.update(ref=ref, train=scene.train, test=scene.test)
+    pool = get_context("fork").Pool(cores) if ref is not None else None
+    for _ in range(args.warmup):
+        cpu_reference_step(ref, scene.train, scene.test, cfg_kw, pool)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        cpu_reference_step(ref, scene.train, scene.test, cfg_kw, pool)
+        times.append(time.perf_counter() - t0)
+    if pool is not None:
+        pool.close()
+    px = (len(scene.train) + n_test) * scene.width * scene.height
+    ms = 1000 * statistics.mean(times)
+    value = px / (ms / 1000) / 1e6
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "Mpx/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (seeded scenes with BASELINE config 3 shapes)",
+        "config": {"workload": "C3 1920x1080 L6 thr0.5: build_background_model(64 train) + "
+                               f"detect_octree({n_test} test) per step (bounded sample of the 256-frame batch)",
+                   "parallelism": f"fork pool x{cores}" if ref is not None else "1 process (oracle port)"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "Mpx/s", "cores": cores if ref is not None else 1,
+                         "kind": "reference" if ref is not None else "port",
+                         "sample": f"64 training + {n_test} test frames per step; per-frame trees and masks in "
+                                   "a fork pool over all host cores, decode + merge serial"},
+        "e2e": {"value": round(value, 3), "unit": "Mpx/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1412_1945_b200 as obg
+    from paper_1412_1945_b200 import scenes
+    from paper_1412_1945_b200.distributed import build_background_model_sharded
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    # weak scaling: every rank gets its own seeded scene shard
+    scene = scenes.generate(CONFIG_ID, seed=args.seed + rank)
+    cfg = scene.config
+    P = scene.width * scene.height
+    n_train, n_test = len(scene.train), len(scene.test)
+    train = torch.from_numpy(scene.train).to(dev)
+    test = torch.from_numpy(scene.test).to(dev)
+    masks = torch.empty((n_test, scene.height, scene.width), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def build():
+        if world > 1:
+            return build_background_model_sharded(train, cfg, global_trees=n_train * world)
+        return obg.build_background_model_device(train, cfg)
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        model = build()
+        if ev is not None:
+            ev[1].record(stream)
+        obg.classify(model, test, out=masks)
+        if ev is not None:
+            ev[2].record(stream)
+        return model
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for k in range(args.steps):
+        model = step(evs[k])
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    total_ms = t_start.elapsed_time(t_end)
+    build_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    cls_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    stats = torch.tensor([total_ms, statistics.mean(build_ms), statistics.mean(cls_ms)], dtype=torch.float64,
+                         device=dev)
+    if world > 1:
+        dist.all_reduce(stats, op=dist.ReduceOp.MAX)
+    total_ms, build_avg, cls_avg = stats.tolist()
+    ms_per_step = total_ms / args.steps
+    px_step = (n_train + n_test) * P
+    value = px_step * world / (ms_per_step / 1000) / 1e6
+
+    # parity of the timed outputs against the reference's recorded outputs
+    parity = None
+    rec = golden_record()
+    if rank == 0 and rec is not None and args.seed == 1412:
+        blob = model.trees[0][0].to_bytes()
+        m = masks.cpu().numpy()
+        ok_tree = hashlib.sha256(blob).hexdigest() == rec["merged_sha"]
+        ok_masks = all(hashlib.sha256(np.packbits(m[i].astype(bool).ravel(), bitorder="little").tobytes())
+                       .hexdigest() == rec["mask_sha"][i] for i in range(n_test)) if world == 1 else None
+        parity = {"merged_tree_vs_reference": ok_tree if world == 1 else None, "masks_vs_reference": ok_masks,
+                  "frames": n_test}
+
+    # end to end through the public API: pinned host frames -> device -> host masks
+    e2e = None
+    if not args.no_e2e:
+        h_train = torch.from_numpy(scene.train).pin_memory()
+        h_test = torch.from_numpy(scene.test).pin_memory()
+        h_masks = torch.empty((n_test, scene.height, scene.width), dtype=torch.uint8).pin_memory()
+
+        def e2e_step():
+            if world > 1:
+                model = build_background_model_sharded(h_train.to(dev, non_blocking=True), cfg,
+                                                       global_trees=n_train * world)
+            else:
+                model = obg.build_background_model(h_train, cfg)
+            out = obg.classify(model, h_test.to(dev, non_blocking=True), out=masks)
+            h_masks.copy_(out, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        e_steps = max(3, min(args.steps, 10))
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        a.record(stream)
+        for _ in range(e_steps):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        e_ms = torch.tensor([a.elapsed_time(b) / e_steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        e_ms = float(e_ms.item())
+        e2e = {"value": round(px_step * world / (e_ms / 1000) / 1e6, 3), "unit": "Mpx/s",
+               "h2d_bytes_per_step": int(h_train.numel() + h_test.numel()),
+               "d2h_bytes_per_step": int(h_masks.numel()), "ms_per_step": round(e_ms, 3),
+               "path": "build_background_model(pinned host frames) + classify(host->device test batch) + "
+                       "mask D2H into pinned host memory"}
+
+    peak, peak_src = peaks()
+    cls_bytes = n_test * P * 4                 # 3 B read + 1 B mask written per pixel
+    build_bytes = n_train * (P * 3 + obg._lib.cube_words(cfg.levels) * 4)
+    cls_gbs = cls_bytes / (cls_avg / 1000) / 1e9
+    build_gbs = build_bytes / (build_avg / 1000) / 1e9
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(scene, dict(levels=cfg.levels, threshold=cfg.threshold, training_frames=n_train))
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "Mpx/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (seeded scenes with BASELINE config 3 shapes: gradient + N(0,3) noise, 20% "
+                    "bimodal swaying rows, 10% bootstrapped training frames, 8 moving ellipses)",
+            "config": {"workload": "C3 1920x1080 L6 thr0.5: build model from 64 training frames + classify "
+                                   "256 test frames per step (per rank)",
+                       "frames_per_step": n_train + n_test, "pixels_per_step": px_step * world,
+                       "parallelism": f"dp{world}" + (" (NCCL all-reduce of merge counts)" if world > 1 else ""),
+                       "l2": f"inputs {(n_train + n_test) * P * 3 / 2**30:.2f} GiB per step > 126 MB L2 "
+                             "(no flush needed)",
+                       "build_ms": round(build_avg, 4), "classify_ms": round(cls_avg, 4),
+                       "build_mpx_s": round(n_train * P / (build_avg / 1000) / 1e6, 1),
+                       "classify_mpx_s": round(n_test * P / (cls_avg / 1000) / 1e6, 1),
+                       "build_hbm_frac": round(build_gbs / peak, 4)},
+            "roofline": {"bound": "hbm", "kernel": "k_classify_flat<6> (obg_classify)",
+                         "achieved": round(cls_gbs, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(cls_gbs / peak, 4), "traffic": None, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": cls_bytes,
+                         "bytes_per_unit": "4 B/px (3 read + 1 mask byte written) x 256 x 1920x1080"},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps * (6 if world > 1 else 5),
+            "gpu_launches_per_step": {"k_build_flat": 1, "k_pyramid": 1,
+                                      "k_merge" if world == 1 else "k_merge+k_threshold": 1 if world == 1 else 2,
+                                      "k_leaf_cube": 1, "k_classify_flat": 1},
+            "clocks": clk,
+            "parity": parity,
+            "gpu": torch.cuda.get_device_name(dev),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

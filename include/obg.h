@@ -1,0 +1,141 @@
+/*
+ * obg.h -- C ABI of the B200 octree background-model hot path (libobg.so).
+ *
+ * Drop-in boundary for the octabg reference's build / prune / merge / classify
+ * path (reference: /root/reference/pkg/src/octabg/).  Every entry point takes
+ * plain device pointers and sizes plus a CUDA stream handle (`void*` holding a
+ * cudaStream_t, NULL = legacy default stream).  Buffers are caller-allocated
+ * and caller-owned; the library holds no persistent allocations and no global
+ * mutable state other than a per-device launch-configuration cache, so calls
+ * on different streams/threads are safe.
+ *
+ * Status: 0 = OK, negative = error (see OBG_E*).  obg_last_error() returns a
+ * thread-local message for the last failing call on the calling thread.
+ *
+ * Data layout:
+ *   frames   u8  [n_frames][height][width][3]  (HWC RGB, the reference's
+ *                                               (h, w, 3) uint8 frames)
+ *   pyramid  u32 [obg_pyramid_words(L)]        one octree = per-level presence
+ *            bitsets, level 1..L concatenated (level l at
+ *            obg_level_offset(L, l)); bit c of level l <=> the node whose
+ *            path code (octree.py:70-80, l octal digits) is c exists.  Level-l
+ *            word count = max(1, 8^l / 32).  The child mask byte of node p at
+ *            level l (octree.py:217-227) is byte p of level l+1.
+ *   cube     u32 [obg_cube_words(L)]           kernel-internal leaf bitset in
+ *            "RGB cube" order: idx = R'<<2L | G'<<L | B' with C' = C >> (8-L).
+ *   mask     u8  [n_frames][height][width]     0/1 (numpy bool layout), or
+ *            bit-packed u8 [n_frames][ceil(h*w/8)], LSB-first per frame.
+ */
+#ifndef OBG_H
+#define OBG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OBG_OK            0
+#define OBG_EINVAL       -1   /* bad argument (maps to ValueError) */
+#define OBG_EUNSUPPORTED -2   /* valid but unsupported configuration */
+#define OBG_ECUDA        -3   /* CUDA runtime / launch failure */
+
+#define OBG_MASK_U8     0
+#define OBG_MASK_PACKED 1
+
+/* ABI version of this header (bumped on incompatible change). */
+int obg_abi_version(void);
+
+/* Thread-local description of the last error on this thread ("" if none). */
+const char* obg_last_error(void);
+
+/* Sizes of the layouts above, in 32-bit words.  levels in 1..8, else -1. */
+int64_t obg_pyramid_words(int levels);
+int64_t obg_level_offset(int levels, int level);
+int64_t obg_cube_words(int levels);
+
+/* Scratch needed by obg_build_presence, in bytes. */
+int64_t obg_build_workspace_bytes(int n_trees, int n_regions, int levels);
+
+/* Path code per pixel, reference octree order.
+ * Replaces pack_codes (octree.py:83-90): codes[i] = (SPREAD_R[r] | SPREAD_G[g]
+ * | SPREAD_B[b]) >> 3*(8-levels) for pixel i = pixels[3i..3i+2]. */
+int obg_pack_codes(const uint8_t* pixels, int64_t n_pixels, int levels,
+                   uint32_t* codes, void* stream);
+
+/* Per-(group, region) presence octrees of a batch of training frames.
+ * Replaces the build loop of build_background_model (model.py:166-179) and
+ * build_frame_tree (model.py:93-109): frames are split into
+ * n_groups = n_frames / group_size consecutive groups (a trailing partial
+ * group is dropped, model.py:166-167); each group and grid region
+ * (region_bounds, model.py:69-75) yields one tree holding every quantized
+ * colour its pixels carry.
+ *   out_pyramids : u32 [n_groups][grid_rows*grid_cols][obg_pyramid_words(L)]
+ *   out_counts   : optional (NULL = skip) u32 [n_groups][R*C][8^L], per-leaf
+ *                  pixel occupancy histogram in path-code order (a superset of
+ *                  the reference, which stores presence only; oracle is
+ *                  np.bincount(pack_codes(block)))
+ *   workspace    : >= obg_build_workspace_bytes(n_groups, R*C, L) bytes. */
+int obg_build_presence(const uint8_t* frames, int n_frames, int height, int width,
+                       int levels, int grid_rows, int grid_cols, int group_size,
+                       uint32_t* out_pyramids, uint32_t* out_counts,
+                       void* workspace, int64_t workspace_bytes, void* stream);
+
+/* Pyramids from leaf-level bitsets (path-code order, max(1,8^L/32) words per
+ * tree): every interior level is the OR-reduction of the level below, i.e.
+ * the nodes a tree built by Octree.store_code (octree.py:158-169) creates. */
+int obg_pyramid_from_leaves(const uint32_t* leaves, int n_trees, int levels,
+                            uint32_t* out_pyramids, void* stream);
+
+/* Octree.prune (octree.py:193-204, _copy_truncated 284-290) on n_trees
+ * pyramids: the result keeps levels 1..new_levels (dead-end nodes included). */
+int obg_prune(const uint32_t* pyramids, int n_trees, int levels, int new_levels,
+              uint32_t* out_pyramids, void* stream);
+
+/* Per-node tree counts for merge_trees (model.py:112-154).
+ * pyramids: u32 [n_trees][n_regions][PW]; counts: u32 [n_regions][PW*32],
+ * counts[r][w*32+b] = number of input trees of region r holding node (w, b). */
+int obg_merge_counts(const uint32_t* pyramids, int n_trees, int n_regions, int levels,
+                     uint32_t* counts, void* stream);
+
+/* counts >= k_min -> merged pyramids u32 [n_regions][PW].  The host computes
+ * k_min = min{k >= 1 : k / total >= threshold} in IEEE double exactly as
+ * model.py:152 compares. */
+int obg_merge_threshold(const uint32_t* counts, int n_regions, int levels, int64_t k_min,
+                        uint32_t* out_pyramids, void* stream);
+
+/* Fused obg_merge_counts + obg_merge_threshold (single GPU). */
+int obg_merge(const uint32_t* pyramids, int n_trees, int n_regions, int levels,
+              int64_t k_min, uint32_t* out_pyramids, void* stream);
+
+/* Leaf level of n pyramids -> cube-order bitsets u32 [n][obg_cube_words(L)]
+ * (the classify operand; detect.py:46 reads only full-depth leaves). */
+int obg_leaf_cube(const uint32_t* pyramids, int n_trees, int levels,
+                  uint32_t* cube, void* stream);
+
+/* Foreground masks.  Replaces detect_octree (detect.py:22-53): pixel is
+ * foreground iff its quantized colour is not a full-depth leaf of its
+ * region's tree (empty tree => all foreground).
+ *   cube_bits : u32 [grid_rows*grid_cols][obg_cube_words(L)] from obg_leaf_cube
+ *   mask      : OBG_MASK_U8 -> u8 [n][h][w] 0/1; OBG_MASK_PACKED -> u8
+ *               [n][ceil(h*w/8)], pixel i of a frame at bit i%8 of byte i/8. */
+int obg_classify(const uint8_t* frames, int n_frames, int height, int width, int levels,
+                 int grid_rows, int grid_cols, const uint32_t* cube_bits,
+                 uint8_t* mask, int mask_format, void* stream);
+
+/* Preorder child-mask serialization of one pyramid (Octree.to_bytes,
+ * octree.py:217-227, 258-267) computed on the device.
+ *   has_root : 1 if the tree has a root node.
+ *   out      : device buffer of >= 1 + popcount(pyramid) bytes.
+ *   n_out    : host pointer receiving the byte count (synchronises stream).
+ *   workspace: >= obg_serialize_workspace_bytes(L) bytes. */
+int64_t obg_serialize_workspace_bytes(int levels);
+int obg_serialize(const uint32_t* pyramid, int levels, int has_root, uint8_t* out,
+                  int64_t out_capacity, int64_t* n_out, void* workspace,
+                  int64_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OBG_H */

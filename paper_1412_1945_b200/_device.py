@@ -1,0 +1,74 @@
+"""Device plumbing: PyTorch is used only as the CUDA buffer / stream carrier."""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+        _torch = t
+    return _torch
+
+
+def require_cuda() -> None:
+    """Fail loudly: the octree hot path has no CPU implementation."""
+    _lib.load()
+    if not torch().cuda.is_available():
+        raise RuntimeError("the octree hot path needs a CUDA device (B200); none is visible")
+
+
+def stream_handle() -> int:
+    return torch().cuda.current_stream().cuda_stream
+
+
+def ptr(t) -> int:
+    return t.data_ptr()
+
+
+def empty(shape, dtype_name: str):
+    t = torch()
+    return t.empty(shape, dtype=getattr(t, dtype_name), device="cuda")
+
+
+def zeros(shape, dtype_name: str):
+    t = torch()
+    return t.zeros(shape, dtype=getattr(t, dtype_name), device="cuda")
+
+
+def to_device_u8(frames):
+    """A contiguous uint8 CUDA tensor view/copy of ``frames`` (numpy or torch)."""
+    t = torch()
+    if isinstance(frames, t.Tensor):
+        if frames.dtype != t.uint8:
+            raise ValueError(f"expected uint8 frames, got {frames.dtype}")
+        x = frames if frames.is_cuda else frames.to("cuda", non_blocking=frames.is_pinned())
+        return x.contiguous()
+    arr = np.ascontiguousarray(frames)
+    return t.from_numpy(arr).to("cuda")
+
+
+def to_device_u32(arr):
+    t = torch()
+    if isinstance(arr, t.Tensor):
+        return arr.to("cuda").contiguous()
+    a = np.ascontiguousarray(arr, dtype=np.uint32)
+    return t.from_numpy(a.view(np.int32)).to("cuda")
+
+
+def u32_to_numpy(tensor) -> np.ndarray:
+    """Device int32-typed words -> host uint32 ndarray."""
+    return tensor.detach().cpu().numpy().view(np.uint32)
+
+
+def is_tensor(x) -> bool:
+    try:
+        return isinstance(x, torch().Tensor)
+    except ImportError:  # pragma: no cover
+        return False

@@ -1,0 +1,946 @@
+// obg.cu -- sm_100a kernels + C ABI for the octree background-model hot path.
+//
+// Reference being replaced (PUBLIC reference, /root/reference/pkg/src/octabg):
+//   pack_codes           octree.py:83-90
+//   build_frame_tree     model.py:93-109   (np.unique + Octree.store_code loop)
+//   build_background_model model.py:157-185
+//   merge_trees          model.py:112-154
+//   Octree.prune         octree.py:193-204
+//   Octree.to_bytes      octree.py:217-227, 258-267
+//   detect_octree        detect.py:22-53
+//
+// Design: everything is byte/bit streaming and HBM-bound.  The
+// streaming kernels (build, classify) never materialise path codes: each pixel
+// is mapped to a "cube" index idx = R'<<2L | G'<<L | B' (C' = C >> (8-L)),
+// which costs one PRMT + 3 shifts + 2 LOP3 per pixel instead of the 3-way bit
+// interleave of the reference code.  Cube-order bitsets are converted to the
+// reference's octree (path-code) order only at tree granularity (<= 2^21 bits),
+// where the per-level pyramid, merge and serialisation live.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+#include <stdarg.h>
+
+#include "../../include/obg.h"
+
+#define OBG_ABI_VERSION 1
+
+// ---------------------------------------------------------------------------
+// error plumbing
+// ---------------------------------------------------------------------------
+static thread_local char g_err[512];
+
+static int set_err(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                              \
+  do {                                                                              \
+    cudaError_t _e = (expr);                                                        \
+    if (_e != cudaSuccess)                                                          \
+      return set_err(OBG_ECUDA, "%s failed: %s", #expr, cudaGetErrorString(_e));   \
+  } while (0)
+
+#define LAUNCH_CHECK(name)                                                          \
+  do {                                                                              \
+    cudaError_t _e = cudaGetLastError();                                            \
+    if (_e != cudaSuccess)                                                          \
+      return set_err(OBG_ECUDA, "launch of %s failed: %s", name, cudaGetErrorString(_e)); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// layout helpers (host + device)
+// ---------------------------------------------------------------------------
+__host__ __device__ static constexpr int64_t level_words(int l) {
+  // level l holds 8^l bits; at least one word.
+  return l <= 1 ? 1 : (int64_t(1) << (3 * l - 5));
+}
+__host__ __device__ static constexpr int64_t level_offset(int l) {
+  // word offset of level l (1-based) inside a pyramid
+  int64_t off = 0;
+  for (int m = 1; m < l; ++m) off += level_words(m);
+  return off;
+}
+__host__ __device__ static constexpr int64_t pyr_words(int L) { return level_offset(L + 1); }
+__host__ __device__ static constexpr int64_t cube_words(int L) { return level_words(L); }
+
+// bit i of v -> bit 3i (v < 256)
+__host__ __device__ static inline uint32_t spread3(uint32_t v) {
+  v = (v | (v << 8)) & 0x0000F00Fu;
+  v = (v | (v << 4)) & 0x000C30C3u;
+  v = (v | (v << 2)) & 0x00249249u;
+  return v;
+}
+// bit 3i of v -> bit i
+__host__ __device__ static inline uint32_t compact3(uint32_t v) {
+  v &= 0x00249249u;
+  v = (v | (v >> 2)) & 0x000C30C3u;
+  v = (v | (v >> 4)) & 0x0000F00Fu;
+  v = (v | (v >> 8)) & 0x000000FFu;
+  return v;
+}
+// cube index -> path code (octree.py:21-35: R bit i -> 3i+2, G -> 3i+1, B -> 3i)
+__host__ __device__ static inline uint32_t cube_to_code(uint32_t idx, int L) {
+  uint32_t m = (1u << L) - 1u;
+  uint32_t r = (idx >> (2 * L)) & m, g = (idx >> L) & m, b = idx & m;
+  return (spread3(r) << 2) | (spread3(g) << 1) | spread3(b);
+}
+__host__ __device__ static inline uint32_t code_to_cube(uint32_t code, int L) {
+  return (compact3(code >> 2) << (2 * L)) | (compact3(code >> 1) << L) | compact3(code);
+}
+
+// x holds bytes [*, R, G, B] (byte 0 ignored).  Returns R'<<2L | G'<<L | B'.
+template <int L>
+__device__ __forceinline__ uint32_t cube_idx(uint32_t x) {
+  constexpr int s = 8 - L;
+  constexpr uint32_t M = (1u << L) - 1u;
+  uint32_t c3 = x >> (24 + s);                              // B' -> [0, L)
+  uint32_t c2 = (x >> (24 - 2 * L)) & (M << L);             // G' -> [L, 2L)
+  uint32_t c1;
+  if constexpr (3 * L >= 16) c1 = (x << (3 * L - 16)) & (M << (2 * L));  // R' -> [2L, 3L)
+  else c1 = (x >> (16 - 3 * L)) & (M << (2 * L));
+  return c1 | c2 | c3;
+}
+
+// Pixel j (0..15) of a 48-byte unit held in w[0..11] -> [*, R, G, B]
+template <int J>
+__device__ __forceinline__ uint32_t pixel_word(const uint32_t (&w)[12]) {
+  constexpr int o = 3 * J, a = o >> 2, b = o & 3;
+  constexpr uint32_t sel = (uint32_t(b) << 4) | (uint32_t(b + 1) << 8) | (uint32_t(b + 2) << 12);
+  if constexpr (a + 1 < 12) return __byte_perm(w[a], w[a + 1], sel);
+  else return __byte_perm(w[a], w[a], sel);
+}
+
+__device__ __forceinline__ uint32_t rgb_word_scalar(const uint8_t* p) {
+  return (uint32_t(p[0]) << 8) | (uint32_t(p[1]) << 16) | (uint32_t(p[2]) << 24);
+}
+
+__device__ __forceinline__ void load_unit(const uint8_t* __restrict__ base, int64_t u, uint32_t (&w)[12]) {
+  const uint4* p = reinterpret_cast<const uint4*>(base) + 3 * u;
+  uint4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+  w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+  w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+  w[8] = c.x; w[9] = c.y; w[10] = c.z; w[11] = c.w;
+}
+
+// ---------------------------------------------------------------------------
+// device properties cache
+// ---------------------------------------------------------------------------
+static int g_sm_count[64];
+
+static int sm_count() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (dev < 0 || dev >= 64) return 148;
+  if (g_sm_count[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    g_sm_count[dev] = n;
+  }
+  return g_sm_count[dev];
+}
+
+template <typename K>
+static int occupancy(K kernel, int block, size_t smem) {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, block, smem) != cudaSuccess || n <= 0) n = 1;
+  return n;
+}
+
+// ===========================================================================
+// K1  build: frames -> cube-order presence bitsets (workspace)
+// ===========================================================================
+// Flat path: 1x1 grid, frame pixels % 16 == 0, 16-byte aligned frames.  Each
+// CTA owns a contiguous range of 16-pixel units, keeps a private shared-memory
+// cube bitset (check-before-set: an ATOMS only when the bit is new to this
+// CTA), and ORs the non-zero words into the tree's workspace bitset whenever
+// its range crosses a tree (group) boundary.
+constexpr int BUILD_BLOCK = 512;
+
+template <int L, bool SMEM_BITS>
+__device__ __forceinline__ void set_bit(uint32_t* bits, uint32_t idx) {
+  uint32_t* wp = bits + (idx >> 5);
+  uint32_t wd;
+  if constexpr (SMEM_BITS) wd = *wp;
+  else wd = *reinterpret_cast<volatile uint32_t*>(wp);
+  if (!((wd >> (idx & 31u)) & 1u)) atomicOr(wp, 1u << (idx & 31u));
+}
+
+template <int L>
+__device__ __forceinline__ void count_code(uint32_t* counts, uint32_t idx) {
+  uint32_t code = cube_to_code(idx, L);
+  unsigned peers = __match_any_sync(__activemask(), code);
+  int leader = __ffs(peers) - 1;
+  if ((threadIdx.x & 31) == leader) atomicAdd(counts + code, (uint32_t)__popc(peers));
+}
+
+template <int L, bool SMEM_BITS, bool COUNTS>
+__global__ void __launch_bounds__(BUILD_BLOCK)
+k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t total_units,
+             int group_size, int64_t units_per_cta, uint32_t* __restrict__ ws,
+             uint32_t* __restrict__ counts) {
+  extern __shared__ uint32_t s_bits[];
+  constexpr int64_t CW = cube_words(L);
+  const int64_t u_begin = int64_t(blockIdx.x) * units_per_cta;
+  const int64_t u_end = min(total_units, u_begin + units_per_cta);
+  if (u_begin >= u_end) return;
+  if constexpr (SMEM_BITS) {
+    for (int i = threadIdx.x; i < CW; i += BUILD_BLOCK) s_bits[i] = 0u;
+    __syncthreads();
+  }
+  const int64_t units_per_tree = units_per_frame * group_size;
+  int64_t u = u_begin;
+  while (u < u_end) {
+    const int64_t tree = u / units_per_tree;
+    const int64_t seg_end = min(u_end, (tree + 1) * units_per_tree);
+    uint32_t* bits;
+    if constexpr (SMEM_BITS) bits = s_bits;
+    else bits = ws + tree * CW;
+    uint32_t* cnt = COUNTS ? counts + tree * (int64_t(1) << (3 * L)) : nullptr;
+    for (int64_t v = u + threadIdx.x; v < seg_end; v += BUILD_BLOCK) {
+      uint32_t w[12];
+      load_unit(frames, v, w);
+      uint32_t idx[16];
+      idx[0] = cube_idx<L>(pixel_word<0>(w));   idx[1] = cube_idx<L>(pixel_word<1>(w));
+      idx[2] = cube_idx<L>(pixel_word<2>(w));   idx[3] = cube_idx<L>(pixel_word<3>(w));
+      idx[4] = cube_idx<L>(pixel_word<4>(w));   idx[5] = cube_idx<L>(pixel_word<5>(w));
+      idx[6] = cube_idx<L>(pixel_word<6>(w));   idx[7] = cube_idx<L>(pixel_word<7>(w));
+      idx[8] = cube_idx<L>(pixel_word<8>(w));   idx[9] = cube_idx<L>(pixel_word<9>(w));
+      idx[10] = cube_idx<L>(pixel_word<10>(w)); idx[11] = cube_idx<L>(pixel_word<11>(w));
+      idx[12] = cube_idx<L>(pixel_word<12>(w)); idx[13] = cube_idx<L>(pixel_word<13>(w));
+      idx[14] = cube_idx<L>(pixel_word<14>(w)); idx[15] = cube_idx<L>(pixel_word<15>(w));
+#pragma unroll
+      for (int j = 0; j < 16; ++j) set_bit<L, SMEM_BITS>(bits, idx[j]);
+      if constexpr (COUNTS) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) count_code<L>(cnt, idx[j]);
+      }
+    }
+    if constexpr (SMEM_BITS) {
+      __syncthreads();
+      uint32_t* dst = ws + tree * CW;
+      for (int i = threadIdx.x; i < CW; i += BUILD_BLOCK) {
+        uint32_t x = s_bits[i];
+        if (x) { atomicOr(dst + i, x); s_bits[i] = 0u; }
+      }
+      __syncthreads();
+    }
+    u = seg_end;
+  }
+}
+
+// Generic path: any grid, any frame size / alignment.  One thread per pixel,
+// region via region_of (model.py:61-66), bits in the workspace (global).
+template <bool COUNTS>
+__global__ void __launch_bounds__(256)
+k_build_generic(const uint8_t* __restrict__ frames, int64_t n_pixels_used, int H, int W, int L,
+                int R, int C, int group_size, uint32_t* __restrict__ ws, uint32_t* __restrict__ counts) {
+  const int64_t P = int64_t(H) * W;
+  const int64_t CW = cube_words(L);
+  const int s = 8 - L;
+  const uint32_t m = (1u << L) - 1u;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n_pixels_used;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t f = i / P, p = i - f * P;
+    const int y = int(p / W), x = int(p - int64_t(y) * W);
+    const int row = min(R - 1, int(int64_t(y) * R / H));
+    const int col = min(C - 1, int(int64_t(x) * C / W));
+    const int64_t tree = (f / group_size) * (int64_t(R) * C) + int64_t(row) * C + col;
+    const uint8_t* px = frames + 3 * i;
+    const uint32_t idx = ((uint32_t(px[0]) >> s) << (2 * L)) | ((uint32_t(px[1]) >> s) << L) |
+                         ((uint32_t(px[2]) >> s) & m);
+    uint32_t* wp = ws + tree * CW + (idx >> 5);
+    if (!((*reinterpret_cast<volatile uint32_t*>(wp) >> (idx & 31u)) & 1u)) atomicOr(wp, 1u << (idx & 31u));
+    if (COUNTS) {
+      uint32_t code = cube_to_code(idx, L);
+      atomicAdd(counts + tree * (int64_t(1) << (3 * L)) + code, 1u);
+    }
+  }
+}
+
+// ===========================================================================
+// K2  pyramid: cube-order (or leaf-level path-order) bitsets -> path-order
+//     per-level pyramids.  One CTA per (tree, chunk of <= 1024 leaf words).
+// ===========================================================================
+constexpr int PYR_BLOCK = 256;
+constexpr int PYR_CHUNK = 1024;  // leaf-level words per CTA
+
+// Leaf-level path-order word m (codes 32m..32m+31) from a cube bitset.
+// Codes of one word share all but bits 0..4 = b0 g0 r0 b1 g1; the (b1,b0)
+// quartet is 4 consecutive cube bits, so the word is 8 nibble gathers.
+__device__ __forceinline__ uint32_t morton_word_from_cube(const uint32_t* __restrict__ cube, uint32_t m, int L) {
+  if (L == 1) return cube[0] & 0xFFu;  // cube index == path code for L = 1
+  const uint32_t base = code_to_cube(m << 5, L);
+  uint32_t out = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const uint32_t g0 = c & 1, r0 = (c >> 1) & 1, g1 = (c >> 2) & 1;
+    const uint32_t idx = base + ((g0 | (g1 << 1)) << L) + (r0 << (2 * L));
+    const uint32_t nib = (cube[idx >> 5] >> (idx & 31u)) & 0xFu;
+    const uint32_t sp = (nib & 3u) | ((nib & 12u) << 6);
+    out |= sp << (g0 * 2 + r0 * 4 + g1 * 16);
+  }
+  return out;
+}
+
+// nz4(w): bit q set iff byte q of w is non-zero
+__device__ __forceinline__ uint32_t nz4(uint32_t w) {
+  uint32_t t = w | (w >> 4);
+  t |= t >> 2;
+  t |= t >> 1;
+  t &= 0x01010101u;
+  return (t * 0x10204080u) >> 28;
+}
+
+template <bool FROM_CUBE>
+__global__ void __launch_bounds__(PYR_BLOCK)
+k_pyramid(const uint32_t* __restrict__ src, int64_t src_stride, int L, uint32_t* __restrict__ out) {
+  __shared__ uint32_t s_w[PYR_CHUNK];
+  const int64_t tree = blockIdx.y;
+  const int64_t LW = level_words(L);
+  const int64_t PW = pyr_words(L);
+  const int64_t nw = LW < PYR_CHUNK ? LW : int64_t(PYR_CHUNK);        // words of this chunk at leaf level
+  const int64_t w0 = int64_t(blockIdx.x) * nw;          // first leaf word of the chunk
+  const uint32_t* s = src + tree * src_stride;
+  uint32_t* o = out + tree * PW;
+  // leaf level
+  for (int i = threadIdx.x; i < nw; i += PYR_BLOCK) {
+    uint32_t x;
+    if constexpr (FROM_CUBE) x = morton_word_from_cube(s, uint32_t(w0 + i), L);
+    else x = s[w0 + i];
+    if (L == 1) x &= 0xFFu;
+    s_w[i] = x;
+    if (x) o[level_offset(L) + w0 + i] = x;   // the chunk owns these words
+  }
+  __syncthreads();
+  // bit range of the chunk at the current level: [B, B + n)
+  int64_t B = w0 * 32, n = (L == 1) ? 8 : nw * 32;
+  for (int l = L - 1; l >= 1; --l) {
+    const int64_t off = level_offset(l);
+    if (n >= 256) {            // parent range is whole words, owned by this CTA
+      const int64_t pn = n / 256;
+      uint32_t vals[PYR_CHUNK / 8 / PYR_BLOCK + 1];
+      int cnt = 0;
+      for (int64_t k = threadIdx.x; k < pn; k += PYR_BLOCK) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v |= nz4(s_w[8 * k + q]) << (4 * q);
+        vals[cnt++] = v;
+      }
+      __syncthreads();
+      cnt = 0;
+      for (int64_t k = threadIdx.x; k < pn; k += PYR_BLOCK) {
+        const uint32_t v = vals[cnt++];
+        s_w[k] = v;
+        if (v) o[off + B / 256 + k] = v;
+      }
+      __syncthreads();
+      B /= 8;
+      n /= 8;
+    } else {                   // < 32 parent bits: one partial word, shared
+      if (threadIdx.x == 0) {
+        uint32_t v = 0;
+        if (n >= 32) {
+          for (int q = 0; q < n / 32; ++q) v |= nz4(s_w[q]) << (4 * q);
+        } else {
+          const uint32_t x = s_w[0];
+          if (n >= 8) {
+            for (int q = 0; q < n / 8; ++q) v |= (((x >> (8 * q)) & 0xFFu) != 0u) << q;
+          } else {
+            v = (x & ((1u << n) - 1u)) != 0u;
+          }
+        }
+        s_w[0] = v;
+      }
+      __syncthreads();
+      const int64_t pB = B / 8;
+      const int64_t pn = n >= 8 ? n / 8 : 1;
+      const uint32_t v = s_w[0];
+      if (threadIdx.x == 0 && v) atomicOr(o + off + pB / 32, v << (pB % 32));
+      __syncthreads();
+      B = pB;
+      n = pn;
+    }
+  }
+}
+
+// ===========================================================================
+// K3  merge: per-node counts over trees, threshold k_min
+// ===========================================================================
+// One warp per (region, pyramid word); lane b counts bit b over the trees.
+__global__ void __launch_bounds__(256)
+k_merge(const uint32_t* __restrict__ pyr, int n_trees, int n_regions, int64_t PW, int64_t k_min,
+        uint32_t* __restrict__ counts, uint32_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int64_t total = PW * n_regions;
+  const int64_t tree_stride = PW * n_regions;
+  for (int64_t wi = warp; wi < total; wi += n_warps) {
+    const int64_t r = wi / PW, w = wi - r * PW;
+    const uint32_t* p = pyr + r * PW + w;
+    uint32_t c = 0;
+    int t = 0;
+    for (; t + 4 <= n_trees; t += 4) {
+      const uint32_t a = __ldg(p + (t + 0) * tree_stride), b = __ldg(p + (t + 1) * tree_stride);
+      const uint32_t d = __ldg(p + (t + 2) * tree_stride), e = __ldg(p + (t + 3) * tree_stride);
+      c += ((a >> lane) & 1u) + ((b >> lane) & 1u) + ((d >> lane) & 1u) + ((e >> lane) & 1u);
+    }
+    for (; t < n_trees; ++t) c += (__ldg(p + t * tree_stride) >> lane) & 1u;
+    if (counts) counts[wi * 32 + lane] = c;
+    if (out) {
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, int64_t(c) >= k_min);
+      if (lane == 0) out[wi] = bal;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256)
+k_threshold(const uint32_t* __restrict__ counts, int64_t total_words, int64_t k_min, uint32_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t wi = warp; wi < total_words; wi += n_warps) {
+    const uint32_t c = counts[wi * 32 + lane];
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, int64_t(c) >= k_min);
+    if (lane == 0) out[wi] = bal;
+  }
+}
+
+// ===========================================================================
+// prune / leaf->cube
+// ===========================================================================
+__global__ void k_prune(const uint32_t* __restrict__ pyr, int64_t PW, int64_t PW2, int64_t n_trees,
+                        uint32_t* __restrict__ out) {
+  const int64_t total = PW2 * n_trees;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = i / PW2, w = i - t * PW2;
+    out[i] = pyr[t * PW + w];
+  }
+}
+
+__global__ void k_leaf_cube(const uint32_t* __restrict__ pyr, int64_t PW, int L, int64_t n_trees,
+                            uint32_t* __restrict__ cube) {
+  const int64_t CW = cube_words(L);
+  const int64_t off = level_offset(L);
+  const int64_t total = CW * n_trees;
+  const int nbits = L == 1 ? 8 : 32;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = i / CW, cw = i - t * CW;
+    const uint32_t* leaf = pyr + t * PW + off;
+    uint32_t v = 0;
+    for (int b = 0; b < nbits; ++b) {
+      const uint32_t code = cube_to_code(uint32_t(cw * 32 + b), L);
+      v |= ((__ldg(leaf + (code >> 5)) >> (code & 31u)) & 1u) << b;
+    }
+    cube[i] = v;
+  }
+}
+
+// ===========================================================================
+// K4  classify
+// ===========================================================================
+constexpr int CLS_BLOCK = 256;
+
+// Flat path: 1x1 grid, leaf cube bitset in shared memory (L <= 6) or read
+// through L1/L2 (L >= 7).  One thread = one 16-pixel unit per iteration:
+// 3 x 16-byte loads, 16 lookups, one 16-byte (u8) or 2-byte (packed) store.
+template <int L, bool SMEM_BITS, bool PACKED>
+__global__ void __launch_bounds__(CLS_BLOCK)
+k_classify_flat(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_pixels,
+                const uint32_t* __restrict__ cube, uint8_t* __restrict__ mask) {
+  extern __shared__ uint32_t s_bits[];
+  constexpr int64_t CW = cube_words(L);
+  const uint32_t* bits = cube;
+  if constexpr (SMEM_BITS) {
+    for (int i = threadIdx.x; i < CW; i += CLS_BLOCK) s_bits[i] = __ldg(cube + i);
+    __syncthreads();
+    bits = s_bits;
+  }
+  const int64_t stride = int64_t(gridDim.x) * CLS_BLOCK;
+  for (int64_t u = int64_t(blockIdx.x) * CLS_BLOCK + threadIdx.x; u < n_units; u += stride) {
+    uint32_t w[12];
+    load_unit(frames, u, w);
+    uint32_t idx[16];
+    idx[0] = cube_idx<L>(pixel_word<0>(w));   idx[1] = cube_idx<L>(pixel_word<1>(w));
+    idx[2] = cube_idx<L>(pixel_word<2>(w));   idx[3] = cube_idx<L>(pixel_word<3>(w));
+    idx[4] = cube_idx<L>(pixel_word<4>(w));   idx[5] = cube_idx<L>(pixel_word<5>(w));
+    idx[6] = cube_idx<L>(pixel_word<6>(w));   idx[7] = cube_idx<L>(pixel_word<7>(w));
+    idx[8] = cube_idx<L>(pixel_word<8>(w));   idx[9] = cube_idx<L>(pixel_word<9>(w));
+    idx[10] = cube_idx<L>(pixel_word<10>(w)); idx[11] = cube_idx<L>(pixel_word<11>(w));
+    idx[12] = cube_idx<L>(pixel_word<12>(w)); idx[13] = cube_idx<L>(pixel_word<13>(w));
+    idx[14] = cube_idx<L>(pixel_word<14>(w)); idx[15] = cube_idx<L>(pixel_word<15>(w));
+    uint32_t v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      uint32_t wd;
+      if constexpr (SMEM_BITS) wd = bits[idx[j] >> 5];
+      else wd = __ldg(bits + (idx[j] >> 5));
+      v[j] = __funnelshift_r(wd, wd, idx[j]);      // bit 0 = background
+    }
+    if constexpr (!PACKED) {
+      uint4 o;
+      o.x = __byte_perm(__byte_perm(v[0], v[1], 0x0040), __byte_perm(v[2], v[3], 0x0040), 0x5410);
+      o.y = __byte_perm(__byte_perm(v[4], v[5], 0x0040), __byte_perm(v[6], v[7], 0x0040), 0x5410);
+      o.z = __byte_perm(__byte_perm(v[8], v[9], 0x0040), __byte_perm(v[10], v[11], 0x0040), 0x5410);
+      o.w = __byte_perm(__byte_perm(v[12], v[13], 0x0040), __byte_perm(v[14], v[15], 0x0040), 0x5410);
+      o.x = ~o.x & 0x01010101u; o.y = ~o.y & 0x01010101u;
+      o.z = ~o.z & 0x01010101u; o.w = ~o.w & 0x01010101u;
+      __stcs(reinterpret_cast<uint4*>(mask) + u, o);
+    } else {
+      uint32_t b = 0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) b |= (v[j] & 1u) << j;
+      reinterpret_cast<uint16_t*>(mask)[u] = uint16_t(~b & 0xFFFFu);
+    }
+  }
+  // tail pixels (n_pixels not a multiple of 16; u8 layout only)
+  if constexpr (!PACKED) {
+    if (blockIdx.x == 0) {
+      for (int64_t i = n_units * 16 + threadIdx.x; i < n_pixels; i += CLS_BLOCK) {
+        const uint32_t idx = cube_idx<L>(rgb_word_scalar(frames + 3 * i));
+        const uint32_t wd = SMEM_BITS ? bits[idx >> 5] : __ldg(bits + (idx >> 5));
+        mask[i] = uint8_t(((wd >> (idx & 31u)) & 1u) ^ 1u);
+      }
+    }
+  }
+}
+
+// Generic path: any grid / alignment / frame size.  One thread = 8 pixels of
+// one frame (one packed byte, or 8 u8 mask bytes).
+template <bool PACKED>
+__global__ void __launch_bounds__(256)
+k_classify_generic(const uint8_t* __restrict__ frames, int64_t n_frames, int H, int W, int L, int R, int C,
+                   const uint32_t* __restrict__ cube, uint8_t* __restrict__ mask) {
+  const int64_t P = int64_t(H) * W;
+  const int64_t bytes_per_frame = (P + 7) / 8;
+  const int64_t total = bytes_per_frame * n_frames;
+  const int64_t CW = cube_words(L);
+  const int s = 8 - L;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t f = t / bytes_per_frame, q = t - f * bytes_per_frame;
+    uint32_t byte = 0;
+    for (int k = 0; k < 8; ++k) {
+      const int64_t p = q * 8 + k;
+      if (p >= P) break;
+      const int y = int(p / W), x = int(p - int64_t(y) * W);
+      const int row = min(R - 1, int(int64_t(y) * R / H));
+      const int col = min(C - 1, int(int64_t(x) * C / W));
+      const uint8_t* px = frames + 3 * (f * P + p);
+      const uint32_t idx = ((uint32_t(px[0]) >> s) << (2 * L)) | ((uint32_t(px[1]) >> s) << L) |
+                           (uint32_t(px[2]) >> s);
+      const uint32_t* bits = cube + (int64_t(row) * C + col) * CW;
+      const uint32_t fg = ((__ldg(bits + (idx >> 5)) >> (idx & 31u)) & 1u) ^ 1u;
+      if (PACKED) byte |= fg << k;
+      else mask[f * P + p] = uint8_t(fg);
+    }
+    if (PACKED) mask[t] = uint8_t(byte);
+  }
+}
+
+// ===========================================================================
+// pack_codes
+// ===========================================================================
+__global__ void k_pack_codes(const uint8_t* __restrict__ px, int64_t n, int L, uint32_t* __restrict__ codes) {
+  const int sh = 3 * (8 - L);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const uint8_t* p = px + 3 * i;
+    const uint32_t full = (spread3(p[0]) << 2) | (spread3(p[1]) << 1) | spread3(p[2]);
+    codes[i] = full >> sh;
+  }
+}
+
+// ===========================================================================
+// serialize: preorder child-mask bytes from a pyramid
+// ===========================================================================
+// Preorder position of node (l, p) (l = 0 is the root):
+//   pos = sum_{m<l} (rank_m(p >> 3(l-m)) + 1) + sum_{m>=l} rank_m(p << 3(m-l))
+// where rank_m(q) = number of level-m nodes with code < q.  Node (l, p) emits
+// byte p of level l+1 (its child mask), leaves emit 0 (octree.py:258-267).
+__global__ void k_scan_pyramid(const uint32_t* __restrict__ pyr, int L, uint32_t* __restrict__ prefix,
+                               uint32_t* __restrict__ total) {
+  // single CTA (1024 threads): exclusive popcount prefix per level
+  __shared__ uint32_t s_sum[1024];
+  __shared__ uint32_t s_carry;
+  for (int l = 1; l <= L; ++l) {
+    const int64_t off = level_offset(l), nw = level_words(l);
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < nw; base += 1024) {
+      const int64_t i = base + threadIdx.x;
+      const uint32_t c = i < nw ? __popc(pyr[off + i]) : 0u;
+      s_sum[threadIdx.x] = c;
+      __syncthreads();
+      for (int d = 1; d < 1024; d <<= 1) {
+        uint32_t t = threadIdx.x >= d ? s_sum[threadIdx.x - d] : 0u;
+        __syncthreads();
+        s_sum[threadIdx.x] += t;
+        __syncthreads();
+      }
+      if (i < nw) prefix[off + i] = s_carry + s_sum[threadIdx.x] - c;
+      __syncthreads();
+      if (threadIdx.x == 1023) s_carry += s_sum[1023];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) total[l] = s_carry;
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ uint32_t rank_of(const uint32_t* __restrict__ pyr, const uint32_t* __restrict__ prefix,
+                                            int l, uint64_t q) {
+  const int64_t off = level_offset(l);
+  const uint64_t w = q >> 5;
+  const uint32_t b = uint32_t(q & 31u);
+  const uint32_t word = pyr[off + w];
+  return prefix[off + w] + __popc(b ? (word & ((1u << b) - 1u)) : 0u);
+}
+
+__global__ void k_serialize(const uint32_t* __restrict__ pyr, const uint32_t* __restrict__ prefix, int L,
+                            uint8_t* __restrict__ out) {
+  const int64_t PW = pyr_words(L);
+  for (int64_t gw = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; gw < PW; gw += int64_t(gridDim.x) * blockDim.x) {
+    int l = 1;
+    while (l < L && gw >= level_offset(l + 1)) ++l;
+    const int64_t w = gw - level_offset(l);
+    uint32_t word = pyr[gw];
+    while (word) {
+      const int b = __ffs(word) - 1;
+      word &= word - 1u;
+      const uint64_t p = uint64_t(w) * 32 + b;
+      uint64_t pos = 1;  // the root precedes every node
+      for (int m = 1; m < l; ++m) pos += rank_of(pyr, prefix, m, p >> (3 * (l - m))) + 1;
+      for (int m = l; m <= L; ++m) pos += rank_of(pyr, prefix, m, p << (3 * (m - l)));
+      uint8_t byte = 0;
+      if (l < L) {
+        const uint32_t cw = pyr[level_offset(l + 1) + (p >> 2)];
+        byte = uint8_t(cw >> (8 * (p & 3)));
+      }
+      out[pos] = byte;
+    }
+  }
+}
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+static int grid_for(int64_t work, int block, int max_blocks) {
+  int64_t g = (work + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > max_blocks) g = max_blocks;
+  return int(g);
+}
+
+// C-ABI entry points: C linkage comes from the declarations in obg.h.
+
+int obg_abi_version(void) { return OBG_ABI_VERSION; }
+const char* obg_last_error(void) { return g_err; }
+
+int64_t obg_pyramid_words(int levels) { return (levels < 1 || levels > 8) ? -1 : pyr_words(levels); }
+int64_t obg_level_offset(int levels, int level) {
+  if (levels < 1 || levels > 8 || level < 1 || level > levels) return -1;
+  return level_offset(level);
+}
+int64_t obg_cube_words(int levels) { return (levels < 1 || levels > 8) ? -1 : cube_words(levels); }
+int64_t obg_build_workspace_bytes(int n_trees, int n_regions, int levels) {
+  if (levels < 1 || levels > 8 || n_trees < 0 || n_regions < 1) return -1;
+  return int64_t(n_trees) * n_regions * cube_words(levels) * 4;
+}
+
+int obg_pack_codes(const uint8_t* pixels, int64_t n_pixels, int levels, uint32_t* codes, void* stream) {
+  g_err[0] = 0;
+  if (levels < 1 || levels > 8) return set_err(OBG_EINVAL, "levels must be in 1..8, got %d", levels);
+  if (n_pixels < 0) return set_err(OBG_EINVAL, "n_pixels must be >= 0");
+  if (n_pixels == 0) return OBG_OK;
+  if (!pixels || !codes) return set_err(OBG_EINVAL, "null buffer");
+  k_pack_codes<<<grid_for(n_pixels, 256, sm_count() * 16), 256, 0, as_stream(stream)>>>(pixels, n_pixels, levels, codes);
+  LAUNCH_CHECK("k_pack_codes");
+  return OBG_OK;
+}
+
+template <int L>
+static int launch_build_flat(const uint8_t* frames, int64_t units_per_frame, int64_t total_units, int group_size,
+                             uint32_t* ws, uint32_t* counts, cudaStream_t st) {
+  constexpr bool SMEM = L <= 6;
+  const size_t smem = SMEM ? size_t(cube_words(L)) * 4 : 0;
+  int blocks_per_sm;
+  if (counts) {
+    auto k = k_build_flat<L, SMEM, true>;
+    blocks_per_sm = occupancy(k, BUILD_BLOCK, smem);
+  } else {
+    auto k = k_build_flat<L, SMEM, false>;
+    blocks_per_sm = occupancy(k, BUILD_BLOCK, smem);
+  }
+  const int64_t max_ctas = int64_t(sm_count()) * blocks_per_sm;
+  // at least 4 units per thread per CTA so that tiny inputs use few CTAs
+  int64_t per_cta = (total_units + max_ctas - 1) / max_ctas;
+  const int64_t min_per_cta = int64_t(BUILD_BLOCK) * 4;
+  if (per_cta < min_per_cta) per_cta = min_per_cta;
+  const int grid = int((total_units + per_cta - 1) / per_cta);
+  if (counts)
+    k_build_flat<L, SMEM, true><<<grid, BUILD_BLOCK, smem, st>>>(frames, units_per_frame, total_units, group_size,
+                                                                 per_cta, ws, counts);
+  else
+    k_build_flat<L, SMEM, false><<<grid, BUILD_BLOCK, smem, st>>>(frames, units_per_frame, total_units, group_size,
+                                                                  per_cta, ws, nullptr);
+  LAUNCH_CHECK("k_build_flat");
+  return OBG_OK;
+}
+
+static int launch_pyramid(const uint32_t* src, int64_t src_stride, bool from_cube, int64_t n_trees, int L,
+                          uint32_t* out, cudaStream_t st) {
+  const int64_t LW = level_words(L);
+  const int64_t nw = LW < PYR_CHUNK ? LW : PYR_CHUNK;
+  dim3 grid(unsigned(LW / nw), unsigned(n_trees));
+  if (n_trees > 65535) return set_err(OBG_EUNSUPPORTED, "too many trees in one call (%lld > 65535)", (long long)n_trees);
+  if (from_cube) k_pyramid<true><<<grid, PYR_BLOCK, 0, st>>>(src, src_stride, L, out);
+  else k_pyramid<false><<<grid, PYR_BLOCK, 0, st>>>(src, src_stride, L, out);
+  LAUNCH_CHECK("k_pyramid");
+  return OBG_OK;
+}
+
+int obg_build_presence(const uint8_t* frames, int n_frames, int height, int width, int levels, int grid_rows,
+                       int grid_cols, int group_size, uint32_t* out_pyramids, uint32_t* out_counts, void* workspace,
+                       int64_t workspace_bytes, void* stream) {
+  g_err[0] = 0;
+  if (levels < 1 || levels > 8) return set_err(OBG_EINVAL, "levels must be in 1..8, got %d", levels);
+  if (n_frames < 1) return set_err(OBG_EINVAL, "no frames given");
+  if (height < 1 || width < 1) return set_err(OBG_EINVAL, "frame dimensions must be >= 1");
+  if (grid_rows < 1 || grid_cols < 1) return set_err(OBG_EINVAL, "grid dimensions must be >= 1");
+  if (group_size < 1) return set_err(OBG_EINVAL, "group_size must be >= 1");
+  const int n_groups = n_frames / group_size;
+  if (n_groups == 0)
+    return set_err(OBG_EINVAL, "need at least %d frames for one group, got %d", group_size, n_frames);
+  if (!frames || !out_pyramids || !workspace) return set_err(OBG_EINVAL, "null buffer");
+  const int64_t n_regions = int64_t(grid_rows) * grid_cols;
+  const int64_t n_trees = int64_t(n_groups) * n_regions;
+  const int64_t need = obg_build_workspace_bytes(n_groups, int(n_regions), levels);
+  if (workspace_bytes < need)
+    return set_err(OBG_EINVAL, "workspace too small: %lld < %lld bytes", (long long)workspace_bytes, (long long)need);
+  cudaStream_t st = as_stream(stream);
+  uint32_t* ws = static_cast<uint32_t*>(workspace);
+  const int64_t CW = cube_words(levels);
+  const int64_t PW = pyr_words(levels);
+  CUDA_TRY(cudaMemsetAsync(ws, 0, size_t(n_trees * CW * 4), st));
+  CUDA_TRY(cudaMemsetAsync(out_pyramids, 0, size_t(n_trees * PW * 4), st));
+  if (out_counts) CUDA_TRY(cudaMemsetAsync(out_counts, 0, size_t(n_trees) * (size_t(1) << (3 * levels)) * 4, st));
+
+  const int64_t P = int64_t(height) * width;
+  const int64_t used_pixels = int64_t(n_groups) * group_size * P;
+  const bool flat = n_regions == 1 && (P % 16) == 0 && (reinterpret_cast<uintptr_t>(frames) % 16) == 0;
+  int rc = OBG_OK;
+  if (flat) {
+    const int64_t upf = P / 16, total_units = used_pixels / 16;
+    switch (levels) {
+      case 1: rc = launch_build_flat<1>(frames, upf, total_units, group_size, ws, out_counts, st); break;
+      case 2: rc = launch_build_flat<2>(frames, upf, total_units, group_size, ws, out_counts, st); break;
+      case 3: rc = launch_build_flat<3>(frames, upf, total_units, group_size, ws, out_counts, st); break;
+      case 4: rc = launch_build_flat<4>(frames, upf, total_units, group_size, ws, out_counts, st); break;
+      case 5: rc = launch_build_flat<5>(frames, upf, total_units, group_size, ws, out_counts, st); break;
+      case 6: rc = launch_build_flat<6>(frames, upf, total_units, group_size, ws, out_counts, st); break;
+      case 7: rc = launch_build_flat<7>(frames, upf, total_units, group_size, ws, out_counts, st); break;
+      default: rc = launch_build_flat<8>(frames, upf, total_units, group_size, ws, out_counts, st); break;
+    }
+  } else {
+    const int grid = grid_for(used_pixels, 256, sm_count() * 8);
+    if (out_counts)
+      k_build_generic<true><<<grid, 256, 0, st>>>(frames, used_pixels, height, width, levels, grid_rows, grid_cols,
+                                                   group_size, ws, out_counts);
+    else
+      k_build_generic<false><<<grid, 256, 0, st>>>(frames, used_pixels, height, width, levels, grid_rows, grid_cols,
+                                                    group_size, ws, nullptr);
+    LAUNCH_CHECK("k_build_generic");
+  }
+  if (rc != OBG_OK) return rc;
+  return launch_pyramid(ws, CW, true, n_trees, levels, out_pyramids, st);
+}
+
+int obg_pyramid_from_leaves(const uint32_t* leaves, int n_trees, int levels, uint32_t* out_pyramids, void* stream) {
+  g_err[0] = 0;
+  if (levels < 1 || levels > 8) return set_err(OBG_EINVAL, "levels must be in 1..8, got %d", levels);
+  if (n_trees < 0) return set_err(OBG_EINVAL, "n_trees must be >= 0");
+  if (n_trees == 0) return OBG_OK;
+  if (!leaves || !out_pyramids) return set_err(OBG_EINVAL, "null buffer");
+  cudaStream_t st = as_stream(stream);
+  CUDA_TRY(cudaMemsetAsync(out_pyramids, 0, size_t(n_trees) * pyr_words(levels) * 4, st));
+  return launch_pyramid(leaves, level_words(levels), false, n_trees, levels, out_pyramids, st);
+}
+
+int obg_prune(const uint32_t* pyramids, int n_trees, int levels, int new_levels, uint32_t* out_pyramids, void* stream) {
+  g_err[0] = 0;
+  if (levels < 1 || levels > 8) return set_err(OBG_EINVAL, "levels must be in 1..8, got %d", levels);
+  if (new_levels < 1 || new_levels > levels)
+    return set_err(OBG_EINVAL, "new_depth must be in 1..%d, got %d", levels, new_levels);
+  if (n_trees < 0) return set_err(OBG_EINVAL, "n_trees must be >= 0");
+  if (n_trees == 0) return OBG_OK;
+  if (!pyramids || !out_pyramids) return set_err(OBG_EINVAL, "null buffer");
+  const int64_t PW = pyr_words(levels), PW2 = pyr_words(new_levels);
+  k_prune<<<grid_for(PW2 * n_trees, 256, sm_count() * 8), 256, 0, as_stream(stream)>>>(pyramids, PW, PW2, n_trees,
+                                                                                       out_pyramids);
+  LAUNCH_CHECK("k_prune");
+  return OBG_OK;
+}
+
+static int merge_common(const uint32_t* pyramids, int n_trees, int n_regions, int levels, int64_t k_min,
+                        uint32_t* counts, uint32_t* out, void* stream) {
+  if (levels < 1 || levels > 8) return set_err(OBG_EINVAL, "levels must be in 1..8, got %d", levels);
+  if (n_trees < 1) return set_err(OBG_EINVAL, "no trees to merge");
+  if (n_regions < 1) return set_err(OBG_EINVAL, "n_regions must be >= 1");
+  if (!pyramids) return set_err(OBG_EINVAL, "null buffer");
+  const int64_t PW = pyr_words(levels);
+  const int64_t warps = PW * n_regions;
+  k_merge<<<grid_for(warps * 32, 256, sm_count() * 8), 256, 0, as_stream(stream)>>>(pyramids, n_trees, n_regions, PW,
+                                                                                    k_min, counts, out);
+  LAUNCH_CHECK("k_merge");
+  return OBG_OK;
+}
+
+int obg_merge_counts(const uint32_t* pyramids, int n_trees, int n_regions, int levels, uint32_t* counts, void* stream) {
+  g_err[0] = 0;
+  if (!counts) return set_err(OBG_EINVAL, "null buffer");
+  return merge_common(pyramids, n_trees, n_regions, levels, 0, counts, nullptr, stream);
+}
+
+int obg_merge(const uint32_t* pyramids, int n_trees, int n_regions, int levels, int64_t k_min,
+              uint32_t* out_pyramids, void* stream) {
+  g_err[0] = 0;
+  if (!out_pyramids) return set_err(OBG_EINVAL, "null buffer");
+  if (k_min < 1) return set_err(OBG_EINVAL, "k_min must be >= 1, got %lld", (long long)k_min);
+  return merge_common(pyramids, n_trees, n_regions, levels, k_min, nullptr, out_pyramids, stream);
+}
+
+int obg_merge_threshold(const uint32_t* counts, int n_regions, int levels, int64_t k_min, uint32_t* out_pyramids,
+                        void* stream) {
+  g_err[0] = 0;
+  if (levels < 1 || levels > 8) return set_err(OBG_EINVAL, "levels must be in 1..8, got %d", levels);
+  if (n_regions < 1) return set_err(OBG_EINVAL, "n_regions must be >= 1");
+  if (k_min < 1) return set_err(OBG_EINVAL, "k_min must be >= 1, got %lld", (long long)k_min);
+  if (!counts || !out_pyramids) return set_err(OBG_EINVAL, "null buffer");
+  const int64_t words = pyr_words(levels) * n_regions;
+  k_threshold<<<grid_for(words * 32, 256, sm_count() * 8), 256, 0, as_stream(stream)>>>(counts, words, k_min,
+                                                                                        out_pyramids);
+  LAUNCH_CHECK("k_threshold");
+  return OBG_OK;
+}
+
+int obg_leaf_cube(const uint32_t* pyramids, int n_trees, int levels, uint32_t* cube, void* stream) {
+  g_err[0] = 0;
+  if (levels < 1 || levels > 8) return set_err(OBG_EINVAL, "levels must be in 1..8, got %d", levels);
+  if (n_trees < 0) return set_err(OBG_EINVAL, "n_trees must be >= 0");
+  if (n_trees == 0) return OBG_OK;
+  if (!pyramids || !cube) return set_err(OBG_EINVAL, "null buffer");
+  const int64_t CW = cube_words(levels);
+  k_leaf_cube<<<grid_for(CW * n_trees, 256, sm_count() * 8), 256, 0, as_stream(stream)>>>(
+      pyramids, pyr_words(levels), levels, n_trees, cube);
+  LAUNCH_CHECK("k_leaf_cube");
+  return OBG_OK;
+}
+
+template <int L>
+static int launch_classify_flat(const uint8_t* frames, int64_t n_pixels, const uint32_t* cube, uint8_t* mask,
+                                bool packed, cudaStream_t st) {
+  constexpr bool SMEM = L <= 6;
+  const size_t smem = SMEM ? size_t(cube_words(L)) * 4 : 0;
+  const int64_t n_units = n_pixels / 16;
+  int bps;
+  if (packed) bps = occupancy(k_classify_flat<L, SMEM, true>, CLS_BLOCK, smem);
+  else bps = occupancy(k_classify_flat<L, SMEM, false>, CLS_BLOCK, smem);
+  int64_t grid = int64_t(sm_count()) * bps;
+  const int64_t need = (n_units + CLS_BLOCK - 1) / CLS_BLOCK;
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  if (packed)
+    k_classify_flat<L, SMEM, true><<<unsigned(grid), CLS_BLOCK, smem, st>>>(frames, n_units, n_pixels, cube, mask);
+  else
+    k_classify_flat<L, SMEM, false><<<unsigned(grid), CLS_BLOCK, smem, st>>>(frames, n_units, n_pixels, cube, mask);
+  LAUNCH_CHECK("k_classify_flat");
+  return OBG_OK;
+}
+
+int obg_classify(const uint8_t* frames, int n_frames, int height, int width, int levels, int grid_rows, int grid_cols,
+                 const uint32_t* cube_bits, uint8_t* mask, int mask_format, void* stream) {
+  g_err[0] = 0;
+  if (levels < 1 || levels > 8) return set_err(OBG_EINVAL, "levels must be in 1..8, got %d", levels);
+  if (n_frames < 0) return set_err(OBG_EINVAL, "n_frames must be >= 0");
+  if (height < 1 || width < 1) return set_err(OBG_EINVAL, "frame dimensions must be >= 1");
+  if (grid_rows < 1 || grid_cols < 1) return set_err(OBG_EINVAL, "grid dimensions must be >= 1");
+  if (mask_format != OBG_MASK_U8 && mask_format != OBG_MASK_PACKED)
+    return set_err(OBG_EINVAL, "unknown mask_format %d", mask_format);
+  if (n_frames == 0) return OBG_OK;
+  if (!frames || !cube_bits || !mask) return set_err(OBG_EINVAL, "null buffer");
+  cudaStream_t st = as_stream(stream);
+  const bool packed = mask_format == OBG_MASK_PACKED;
+  const int64_t P = int64_t(height) * width;
+  const int64_t n_pixels = P * n_frames;
+  const bool aligned = (reinterpret_cast<uintptr_t>(frames) % 16) == 0 &&
+                       (reinterpret_cast<uintptr_t>(mask) % (packed ? 2 : 16)) == 0;
+  const bool flat = grid_rows == 1 && grid_cols == 1 && aligned && (!packed || (P % 16) == 0);
+  if (flat) {
+    switch (levels) {
+      case 1: return launch_classify_flat<1>(frames, n_pixels, cube_bits, mask, packed, st);
+      case 2: return launch_classify_flat<2>(frames, n_pixels, cube_bits, mask, packed, st);
+      case 3: return launch_classify_flat<3>(frames, n_pixels, cube_bits, mask, packed, st);
+      case 4: return launch_classify_flat<4>(frames, n_pixels, cube_bits, mask, packed, st);
+      case 5: return launch_classify_flat<5>(frames, n_pixels, cube_bits, mask, packed, st);
+      case 6: return launch_classify_flat<6>(frames, n_pixels, cube_bits, mask, packed, st);
+      case 7: return launch_classify_flat<7>(frames, n_pixels, cube_bits, mask, packed, st);
+      default: return launch_classify_flat<8>(frames, n_pixels, cube_bits, mask, packed, st);
+    }
+  }
+  const int64_t threads = ((P + 7) / 8) * n_frames;
+  const int grid = grid_for(threads, 256, sm_count() * 8);
+  if (packed)
+    k_classify_generic<true><<<grid, 256, 0, st>>>(frames, n_frames, height, width, levels, grid_rows, grid_cols,
+                                                   cube_bits, mask);
+  else
+    k_classify_generic<false><<<grid, 256, 0, st>>>(frames, n_frames, height, width, levels, grid_rows, grid_cols,
+                                                    cube_bits, mask);
+  LAUNCH_CHECK("k_classify_generic");
+  return OBG_OK;
+}
+
+int64_t obg_serialize_workspace_bytes(int levels) {
+  if (levels < 1 || levels > 8) return -1;
+  return (pyr_words(levels) + 16) * 4;
+}
+
+int obg_serialize(const uint32_t* pyramid, int levels, int has_root, uint8_t* out, int64_t out_capacity,
+                  int64_t* n_out, void* workspace, int64_t workspace_bytes, void* stream) {
+  g_err[0] = 0;
+  if (levels < 1 || levels > 8) return set_err(OBG_EINVAL, "levels must be in 1..8, got %d", levels);
+  if (!pyramid || !n_out) return set_err(OBG_EINVAL, "null buffer");
+  if (workspace_bytes < obg_serialize_workspace_bytes(levels) || !workspace)
+    return set_err(OBG_EINVAL, "workspace too small");
+  cudaStream_t st = as_stream(stream);
+  uint32_t* prefix = static_cast<uint32_t*>(workspace);
+  uint32_t* totals = prefix + pyr_words(levels);
+  CUDA_TRY(cudaMemsetAsync(totals, 0, 16 * 4, st));
+  k_scan_pyramid<<<1, 1024, 0, st>>>(pyramid, levels, prefix, totals);
+  LAUNCH_CHECK("k_scan_pyramid");
+  uint32_t h_tot[16];
+  CUDA_TRY(cudaMemcpyAsync(h_tot, totals, sizeof(h_tot), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  int64_t nodes = 0;
+  for (int l = 1; l <= levels; ++l) nodes += h_tot[l];
+  if (!has_root && nodes == 0) { *n_out = 0; return OBG_OK; }
+  const int64_t total = nodes + 1;
+  *n_out = total;
+  if (!out || out_capacity < total)
+    return set_err(OBG_EINVAL, "output capacity %lld < %lld bytes", (long long)out_capacity, (long long)total);
+  // root byte: the level-1 child mask
+  CUDA_TRY(cudaMemcpyAsync(out, pyramid, 1, cudaMemcpyDeviceToDevice, st));
+  const int64_t PW = pyr_words(levels);
+  if (nodes > 0) {
+    k_serialize<<<grid_for(PW, 256, sm_count() * 8), 256, 0, st>>>(pyramid, prefix, levels, out);
+    LAUNCH_CHECK("k_serialize");
+  }
+  return OBG_OK;
+}
+

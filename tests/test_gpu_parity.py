@@ -1,0 +1,288 @@
+"""GPU parity: the CUDA path (through libobg.so's C ABI) against the reference's
+recorded outputs (tests/golden/golden.json) and the CPU oracle.  Integer /
+byte / index work throughout, so every comparison is bit-exact."""
+
+import numpy as np
+import pytest
+
+import paper_1412_1945_b200 as obg
+from cases import random_case_inputs
+from helpers import mask_digest, mask_hex, sha
+from oracle import octree_oracle as orc
+from paper_1412_1945_b200 import ModelConfig, Octree, _lib
+
+pytestmark = pytest.mark.gpu
+
+
+def _cfg(rec, n):
+    return ModelConfig(levels=rec["levels"], threshold=rec["threshold"], grid_rows=rec["grid_rows"],
+                       grid_cols=rec["grid_cols"], group_size=rec["group_size"], training_frames=n)
+
+
+def test_library_loaded_from_tree(cuda):
+    lib = _lib.load()
+    assert lib._name.endswith("paper_1412_1945_b200/_build/libobg.so")
+
+
+@pytest.mark.parametrize("levels", range(1, 9))
+def test_pack_codes(cuda, levels):
+    rng = np.random.default_rng(levels)
+    px = rng.integers(0, 256, size=(37, 29, 3), dtype=np.uint8)
+    assert np.array_equal(obg.pack_codes(px, levels), orc.pack_codes(px, levels))
+
+
+def test_pack_codes_kat(cuda, golden):
+    rng = np.random.default_rng(7)
+    px = rng.integers(0, 256, size=(13, 9, 3), dtype=np.uint8)
+    for L, want in golden["kat"]["pack_codes_13x9"].items():
+        assert obg.pack_codes(px, int(L)).ravel().tolist() == want
+
+
+@pytest.mark.parametrize("case", range(96))
+def test_random_case(cuda, golden, case):
+    rec = golden["random_cases"][case]
+    x = random_case_inputs(case)
+    frames = list(x["frames"])
+    cfg = _cfg(rec, len(frames))
+    R, C, gs = cfg.grid_rows, cfg.grid_cols, cfg.group_size
+    for g in range(len(frames) // gs):
+        for r in range(R):
+            for c in range(C):
+                t = obg.build_frame_tree(frames[g * gs:(g + 1) * gs], (r, c), cfg)
+                assert t.to_bytes().hex() == rec["group_trees"][g][r][c]
+    model = obg.build_background_model(frames, cfg)
+    for r in range(R):
+        for c in range(C):
+            assert model.trees[r][c].to_bytes().hex() == rec["merged"][r][c]
+    for nd, want in rec["pruned00"].items():
+        assert model.trees[0][0].prune(int(nd)).to_bytes().hex() == want
+    for probe, want in zip(x["probes"], rec["masks"]):
+        assert mask_hex(obg.detect_octree(model, probe)) == want
+    assert obg.write_model(model).hex() == rec["model_file"]
+    # merge of host-side trees (the reference's merge_trees API)
+    groups = [obg.build_frame_tree(frames[g * gs:(g + 1) * gs], (0, 0), cfg) for g in range(len(frames) // gs)]
+    host = [Octree.from_bytes(t.to_bytes(), cfg.levels) for t in groups]
+    assert obg.merge_trees(host, cfg.threshold, cfg.levels).to_bytes().hex() == rec["merged"][0][0]
+
+
+@pytest.mark.parametrize("case", range(0, 96, 7))
+def test_counts(cuda, golden, case):
+    rec = golden["random_cases"][case]
+    x = random_case_inputs(case)
+    dev = cuda.from_numpy(np.ascontiguousarray(x["frames"][:1])).cuda()
+    _, cnt = obg.build_presence(dev, rec["levels"], counts=True)
+    assert sha(cnt[0, 0].cpu().numpy().astype(np.int64)) == rec["counts0_sha"]
+
+
+def _check_config(rec, scene, cuda, packed_too=False):
+    assert sha(scene.train) == rec["train_sha"] and sha(scene.test) == rec["test_sha"]
+    cfg = ModelConfig(levels=rec["levels"], threshold=rec["threshold"], training_frames=len(scene.train))
+    train = cuda.from_numpy(scene.train).cuda()
+    model = obg.build_background_model_device(train, cfg)
+    blob = model.trees[0][0].to_bytes()
+    assert len(blob) == rec["merged_len"] and sha(blob) == rec["merged_sha"]
+    assert model.trees[0][0].node_count == rec["merged_nodes"]
+    pyr, cnt = obg.build_presence(train[: len(rec["frame_trees"])], cfg.levels, counts=True)
+    for i, ft in enumerate(rec["frame_trees"]):
+        t = Octree._from_device(pyr[i, 0], cfg.levels)
+        assert sha(t.to_bytes()) == ft["sha"]
+        assert sha(np.asarray(t.leaf_codes(), dtype=np.int64)) == ft["leaf_sha"]
+    assert sha(cnt[0, 0].cpu().numpy().astype(np.int64)) == rec["counts0_sha"]
+    chunk = 32
+    for s in range(0, len(scene.test), chunk):
+        frames = cuda.from_numpy(scene.test[s:s + chunk]).cuda()
+        masks = obg.classify(model, frames).cpu().numpy()
+        for i in range(len(masks)):
+            assert int(masks[i].sum()) == rec["mask_fg"][s + i], f"frame {s + i}"
+            assert mask_digest(masks[i]) == rec["mask_sha"][s + i], f"frame {s + i}"
+        if packed_too:
+            packed = obg.classify(model, frames, packed=True).cpu().numpy()
+            want = np.packbits(masks.reshape(len(masks), -1).astype(bool), axis=1, bitorder="little")
+            assert np.array_equal(packed, want)
+        del frames
+
+
+@pytest.mark.parametrize("cid", [0, 1, 2, 3])
+def test_config(cuda, golden, cid):
+    from paper_1412_1945_b200 import scenes
+    rec = next(r for r in golden["configs"] if r["config"] == cid)
+    _check_config(rec, scenes.generate(cid), cuda, packed_too=cid in (0, 3))
+
+
+@pytest.mark.parametrize("variant", ["constant", "uniform"])
+@pytest.mark.parametrize("levels", [4, 5, 6, 7])
+def test_config4(cuda, golden, variant, levels):
+    from paper_1412_1945_b200 import scenes
+    rec = next(r for r in golden["configs"] if r["config"] == 4 and r["variant"] == variant
+               and r["levels"] == levels)
+    _check_config(rec, scenes.generate(4, levels=levels, variant=variant), cuda)
+
+
+# --- reference behaviours (reference tests/test_detect.py, test_model.py) ------------
+def uniform(h, w, color):
+    return np.full((h, w, 3), color, dtype=np.uint8)
+
+
+def test_training_frame_is_all_background(cuda):
+    rng = np.random.default_rng(5)
+    frame = rng.integers(0, 256, size=(12, 16, 3), dtype=np.uint8)
+    model = obg.build_background_model([frame] * 20, ModelConfig(training_frames=20))
+    assert not obg.detect_octree(model, frame).any()
+
+
+def test_single_deviating_pixel(cuda):
+    frame = uniform(10, 10, (128, 128, 128))
+    model = obg.build_background_model([frame] * 10, ModelConfig(training_frames=10))
+    probe = frame.copy()
+    probe[3, 7] = (0, 0, 0)
+    mask = obg.detect_octree(model, probe)
+    assert mask[3, 7] and mask.sum() == 1 and mask.dtype == np.bool_
+
+
+def test_empty_region_tree_flags_everything(cuda):
+    frames = [uniform(6, 6, (0, 0, 0)), uniform(6, 6, (255, 255, 255))]
+    model = obg.build_background_model(frames, ModelConfig(threshold=1.0, training_frames=2))
+    assert model.trees[0][0].is_empty
+    assert obg.detect_octree(model, uniform(6, 6, (0, 0, 0))).all()
+
+
+def test_static_foreground_absorption(cuda):
+    background = np.full((20, 20, 3), (30, 30, 30), dtype=np.uint8)
+    with_object = background.copy()
+    with_object[5:10, 5:10] = (200, 60, 60)
+    frames = [with_object] * 30 + [background] * 70
+    absorbed = obg.build_background_model(frames, ModelConfig(levels=4, threshold=0.25))
+    rejected = obg.build_background_model(frames, ModelConfig(levels=4, threshold=0.5))
+    assert absorbed.trees[0][0].contains((200, 60, 60))
+    assert not rejected.trees[0][0].contains((200, 60, 60))
+    assert absorbed.trees[0][0].contains((30, 30, 30)) and rejected.trees[0][0].contains((30, 30, 30))
+
+
+def test_trailing_partial_group_discarded(cuda):
+    rng = np.random.default_rng(37)
+    frames = [rng.integers(0, 256, size=(4, 4, 3), dtype=np.uint8) for _ in range(7)]
+    cfg = ModelConfig(levels=3, threshold=0.5, group_size=3, training_frames=7)
+    model = obg.build_background_model(frames, cfg)
+    trees = [obg.build_frame_tree(g, (0, 0), cfg) for g in (frames[0:3], frames[3:6])]
+    assert model.trees[0][0] == obg.merge_trees(trees, 0.5, 3)
+
+
+def test_training_frames_cap(cuda):
+    rng = np.random.default_rng(3)
+    frames = [rng.integers(0, 256, size=(8, 8, 3), dtype=np.uint8) for _ in range(9)]
+    a = obg.build_background_model(frames, ModelConfig(levels=3, threshold=0.4, training_frames=5))
+    b = obg.build_background_model(frames[:5], ModelConfig(levels=3, threshold=0.4, training_frames=5))
+    assert a.trees[0][0] == b.trees[0][0]
+
+
+# --- edge cases of the kernels' fast / generic paths -----------------------------------
+@pytest.mark.parametrize("shape", [(1, 1), (1, 16), (3, 7), (16, 1), (5, 48), (17, 33), (64, 64)])
+@pytest.mark.parametrize("levels", [1, 2, 6, 7, 8])
+def test_shapes_and_levels(cuda, shape, levels):
+    rng = np.random.default_rng(hash((shape, levels)) % 2 ** 32)
+    h, w = shape
+    base = rng.integers(0, 256, size=(1, 1, 1, 3))
+    frames = np.clip(base + rng.integers(-20, 21, size=(9, h, w, 3)), 0, 255).astype(np.uint8)
+    probes = np.clip(base + rng.integers(-30, 31, size=(5, h, w, 3)), 0, 255).astype(np.uint8)
+    cfg = ModelConfig(levels=levels, threshold=0.4, training_frames=9)
+    model = obg.build_background_model(list(frames), cfg)
+    want = orc.build_background_model(list(frames), levels, 0.4)
+    assert model.trees[0][0].to_bytes() == orc.to_bytes(want[(0, 0)])
+    masks = obg.detect_octree_batch(model, probes)
+    for i in range(len(probes)):
+        assert np.array_equal(masks[i], orc.detect_octree(want, probes[i], levels))
+    packed = obg.classify(model, cuda.from_numpy(probes).cuda(), packed=True).cpu().numpy()
+    want_packed = np.packbits(masks.reshape(len(masks), -1), axis=1, bitorder="little")
+    assert np.array_equal(packed, want_packed)
+
+
+def test_misaligned_views_take_generic_path(cuda):
+    rng = np.random.default_rng(11)
+    big = rng.integers(0, 256, size=(6 * 32 * 32 * 3 + 5,), dtype=np.uint8)
+    dev = cuda.from_numpy(big).cuda()
+    frames = dev[5:].view(6, 32, 32, 3)          # 5-byte offset: not 16-byte aligned
+    host = big[5:].reshape(6, 32, 32, 3)
+    cfg = ModelConfig(levels=5, threshold=0.5, training_frames=6)
+    model = obg.build_background_model_device(frames, cfg)
+    want = orc.build_background_model(list(host), 5, 0.5)
+    assert model.trees[0][0].to_bytes() == orc.to_bytes(want[(0, 0)])
+    masks = obg.classify(model, frames).cpu().numpy()
+    for i in range(6):
+        assert np.array_equal(masks[i].astype(bool), orc.detect_octree(want, host[i], 5))
+
+
+@pytest.mark.parametrize("grid", [(1, 1), (2, 2), (3, 1), (1, 5), (7, 9)])
+@pytest.mark.parametrize("gs", [1, 2, 3])
+def test_grids_and_groups(cuda, grid, gs):
+    rng = np.random.default_rng(grid[0] * 100 + grid[1] * 10 + gs)
+    frames = rng.integers(0, 256, size=(8, 6, 10, 3), dtype=np.uint8) // 64 * 64
+    cfg = ModelConfig(levels=3, threshold=0.5, grid_rows=grid[0], grid_cols=grid[1], group_size=gs,
+                      training_frames=8)
+    model = obg.build_background_model(list(frames), cfg)
+    want = orc.build_background_model(list(frames), 3, 0.5, grid[0], grid[1], gs)
+    for r in range(grid[0]):
+        for c in range(grid[1]):
+            assert model.trees[r][c].to_bytes() == orc.to_bytes(want[(r, c)]), (r, c)
+    probe = rng.integers(0, 256, size=(6, 10, 3), dtype=np.uint8) // 64 * 64
+    assert np.array_equal(obg.detect_octree(model, probe), orc.detect_octree(want, probe, 3, grid[0], grid[1]))
+
+
+def test_device_serializer_matches_host(cuda):
+    import ctypes
+    from paper_1412_1945_b200 import _device
+    lib = _lib.load()
+    rng = np.random.default_rng(99)
+    for levels in range(1, 9):
+        for trial in range(3):
+            trees = [orc.tree_from_codes(rng.integers(0, 8 ** levels, size=int(rng.integers(0, 300))), levels)
+                     for _ in range(5)]
+            merged = orc.merge_trees(trees, 0.4, levels) if trial else trees[0]
+            want = orc.to_bytes(merged)
+            t = Octree.from_bytes(want, levels) if want else Octree(levels)
+            dev = t._device()
+            ws_bytes = lib.obg_serialize_workspace_bytes(levels)
+            ws = _device.empty((ws_bytes // 4,), "int32")
+            out = _device.empty((t.node_count + 1,), "uint8")
+            n = ctypes.c_int64(0)
+            _lib.check(lib.obg_serialize(_device.ptr(dev), levels, int(not t.is_empty), _device.ptr(out),
+                                         out.numel(), ctypes.byref(n), _device.ptr(ws), ws_bytes,
+                                         _device.stream_handle()))
+            assert out[: n.value].cpu().numpy().tobytes() == want
+
+
+def test_pyramid_from_leaves_and_prune(cuda):
+    from paper_1412_1945_b200 import _device
+    lib = _lib.load()
+    rng = np.random.default_rng(5)
+    for levels in range(1, 9):
+        codes = rng.integers(0, 8 ** levels, size=500)
+        t = orc.tree_from_codes(codes, levels)
+        leaves = np.zeros(_lib.level_words(levels), dtype=np.uint32)
+        np.bitwise_or.at(leaves, codes >> 5, np.uint32(1) << (codes & 31).astype(np.uint32))
+        dev_leaves = _device.to_device_u32(leaves)
+        out = _device.empty((_lib.pyramid_words(levels),), "int32")
+        _lib.check(lib.obg_pyramid_from_leaves(_device.ptr(dev_leaves), 1, levels, _device.ptr(out),
+                                               _device.stream_handle()))
+        tree = Octree._from_device(out, levels)
+        assert tree.to_bytes() == orc.to_bytes(t)
+        for nd in range(1, levels + 1):
+            assert tree.prune(nd).to_bytes() == orc.to_bytes(orc.prune(t, nd))
+
+
+def test_merge_counts_and_threshold(cuda):
+    from paper_1412_1945_b200 import _device
+    lib = _lib.load()
+    rng = np.random.default_rng(8)
+    levels, n = 4, 11
+    trees = [obg.build_frame_tree([rng.integers(0, 256, size=(9, 9, 3), dtype=np.uint8)], (0, 0),
+                                  ModelConfig(levels=levels)) for _ in range(n)]
+    pyr = cuda.stack([t._device() for t in trees]).unsqueeze(1).contiguous()
+    pw = _lib.pyramid_words(levels)
+    counts = _device.empty((1, pw * 32), "int32")
+    _lib.check(lib.obg_merge_counts(_device.ptr(pyr), n, 1, levels, _device.ptr(counts), _device.stream_handle()))
+    for k_min in (1, 3, 6, 11):
+        out = _device.empty((1, pw), "int32")
+        _lib.check(lib.obg_merge_threshold(_device.ptr(counts), 1, levels, k_min, _device.ptr(out),
+                                           _device.stream_handle()))
+        fused = obg.merge_pyramids(pyr, levels, k_min)
+        assert cuda.equal(out, fused)
