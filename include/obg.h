@@ -102,11 +102,14 @@ int obg_merge_counts(const uint32_t* pyramids, int n_trees, int n_regions, int l
  * k_min = min{k >= 1 : k / total >= threshold} in IEEE double exactly as
  * model.py:152 compares. */
 int obg_merge_threshold(const uint32_t* counts, int n_regions, int levels, int64_t k_min,
-                        uint32_t* out_pyramids, void* stream);
+                        uint32_t* out_pyramids, uint32_t* out_cube, void* stream);
 
-/* Fused obg_merge_counts + obg_merge_threshold (single GPU). */
+/* Fused obg_merge_counts + obg_merge_threshold (single GPU).  For both merge
+ * entry points, out_cube (nullable) additionally receives the merged leaf
+ * level in cube order, u32 [n_regions][obg_cube_words(L)] -- the classify
+ * operand, as obg_leaf_cube would produce it. */
 int obg_merge(const uint32_t* pyramids, int n_trees, int n_regions, int levels,
-              int64_t k_min, uint32_t* out_pyramids, void* stream);
+              int64_t k_min, uint32_t* out_pyramids, uint32_t* out_cube, void* stream);
 
 /* Leaf level of n pyramids -> cube-order bitsets u32 [n][obg_cube_words(L)]
  * (the classify operand; detect.py:46 reads only full-depth leaves). */

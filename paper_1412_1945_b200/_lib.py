@@ -39,8 +39,8 @@ SIGNATURES = {
     "obg_pyramid_from_leaves": (_I, [_P, _I, _I, _P, _P]),
     "obg_prune": (_I, [_P, _I, _I, _I, _P, _P]),
     "obg_merge_counts": (_I, [_P, _I, _I, _I, _P, _P]),
-    "obg_merge_threshold": (_I, [_P, _I, _I, _L, _P, _P]),
-    "obg_merge": (_I, [_P, _I, _I, _I, _L, _P, _P]),
+    "obg_merge_threshold": (_I, [_P, _I, _I, _L, _P, _P, _P]),
+    "obg_merge": (_I, [_P, _I, _I, _I, _L, _P, _P, _P]),
     "obg_leaf_cube": (_I, [_P, _I, _I, _P, _P]),
     "obg_classify": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _P, _I, _P]),
     "obg_serialize_workspace_bytes": (_L, [_I]),

@@ -107,6 +107,25 @@ __device__ __forceinline__ uint32_t cube_idx(uint32_t x) {
   return c1 | c2 | c3;
 }
 
+// Shared-memory bank swizzle of the cube bitset (L = 5, 6).  Word w of the
+// cube holds R'<<(2L-5) | G'<<(L-5) | B'>>5; without a swizzle every R' value
+// lands in the same bank, and a warp reading a colour gradient serialises
+// (ncu r1: 6.6x the ideal shared wavefronts).  phys(w) = w ^ (R' & 31) is an
+// involution that spreads R' over the banks; G' and B'>>5 already vary them.
+template <int L>
+struct Swz {
+  static constexpr bool on = (L == 5 || L == 6);
+  __host__ __device__ static constexpr uint32_t word(uint32_t w) {
+    return on ? (w ^ ((w >> (2 * L - 5)) & 31u)) : w;
+  }
+};
+// same swizzle applied to a bit index computed from x = [*, R, G, B]
+template <int L>
+__device__ __forceinline__ uint32_t swizzle_idx(uint32_t idx, uint32_t x) {
+  if constexpr (Swz<L>::on) return idx ^ ((x >> (11 - L)) & 0x3E0u);
+  else return idx;
+}
+
 // Pixel j (0..15) of a 48-byte unit held in w[0..11] -> [*, R, G, B]
 template <int J>
 __device__ __forceinline__ uint32_t pixel_word(const uint32_t (&w)[12]) {
@@ -205,20 +224,18 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
     for (int64_t v = u + threadIdx.x; v < seg_end; v += BUILD_BLOCK) {
       uint32_t w[12];
       load_unit(frames, v, w);
-      uint32_t idx[16];
-      idx[0] = cube_idx<L>(pixel_word<0>(w));   idx[1] = cube_idx<L>(pixel_word<1>(w));
-      idx[2] = cube_idx<L>(pixel_word<2>(w));   idx[3] = cube_idx<L>(pixel_word<3>(w));
-      idx[4] = cube_idx<L>(pixel_word<4>(w));   idx[5] = cube_idx<L>(pixel_word<5>(w));
-      idx[6] = cube_idx<L>(pixel_word<6>(w));   idx[7] = cube_idx<L>(pixel_word<7>(w));
-      idx[8] = cube_idx<L>(pixel_word<8>(w));   idx[9] = cube_idx<L>(pixel_word<9>(w));
-      idx[10] = cube_idx<L>(pixel_word<10>(w)); idx[11] = cube_idx<L>(pixel_word<11>(w));
-      idx[12] = cube_idx<L>(pixel_word<12>(w)); idx[13] = cube_idx<L>(pixel_word<13>(w));
-      idx[14] = cube_idx<L>(pixel_word<14>(w)); idx[15] = cube_idx<L>(pixel_word<15>(w));
+      uint32_t px[16];
+      px[0] = pixel_word<0>(w);   px[1] = pixel_word<1>(w);   px[2] = pixel_word<2>(w);
+      px[3] = pixel_word<3>(w);   px[4] = pixel_word<4>(w);   px[5] = pixel_word<5>(w);
+      px[6] = pixel_word<6>(w);   px[7] = pixel_word<7>(w);   px[8] = pixel_word<8>(w);
+      px[9] = pixel_word<9>(w);   px[10] = pixel_word<10>(w); px[11] = pixel_word<11>(w);
+      px[12] = pixel_word<12>(w); px[13] = pixel_word<13>(w); px[14] = pixel_word<14>(w);
+      px[15] = pixel_word<15>(w);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) set_bit<L, SMEM_BITS>(bits, idx[j]);
-      if constexpr (COUNTS) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) count_code<L>(cnt, idx[j]);
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t idx = cube_idx<L>(px[j]);
+        set_bit<L, SMEM_BITS>(bits, SMEM_BITS ? swizzle_idx<L>(idx, px[j]) : idx);
+        if constexpr (COUNTS) count_code<L>(cnt, idx);
       }
     }
     if constexpr (SMEM_BITS) {
@@ -226,7 +243,7 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
       uint32_t* dst = ws + tree * CW;
       for (int i = threadIdx.x; i < CW; i += BUILD_BLOCK) {
         uint32_t x = s_bits[i];
-        if (x) { atomicOr(dst + i, x); s_bits[i] = 0u; }
+        if (x) { atomicOr(dst + Swz<L>::word(i), x); s_bits[i] = 0u; }
       }
       __syncthreads();
     }
@@ -268,7 +285,7 @@ k_build_generic(const uint8_t* __restrict__ frames, int64_t n_pixels_used, int H
 //     per-level pyramids.  One CTA per (tree, chunk of <= 1024 leaf words).
 // ===========================================================================
 constexpr int PYR_BLOCK = 256;
-constexpr int PYR_CHUNK = 1024;  // leaf-level words per CTA
+constexpr int PYR_CHUNK = 256;   // leaf-level words per CTA
 
 // Leaf-level path-order word m (codes 32m..32m+31) from a cube bitset.
 // Codes of one word share all but bits 0..4 = b0 g0 r0 b1 g1; the (b1,b0)
@@ -372,43 +389,105 @@ k_pyramid(const uint32_t* __restrict__ src, int64_t src_stride, int L, uint32_t*
 // ===========================================================================
 // K3  merge: per-node counts over trees, threshold k_min
 // ===========================================================================
-// One warp per (region, pyramid word); lane b counts bit b over the trees.
-__global__ void __launch_bounds__(256)
-k_merge(const uint32_t* __restrict__ pyr, int n_trees, int n_regions, int64_t PW, int64_t k_min,
-        uint32_t* __restrict__ counts, uint32_t* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t n_warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  const int64_t total = PW * n_regions;
-  const int64_t tree_stride = PW * n_regions;
-  for (int64_t wi = warp; wi < total; wi += n_warps) {
-    const int64_t r = wi / PW, w = wi - r * PW;
-    const uint32_t* p = pyr + r * PW + w;
-    uint32_t c = 0;
-    int t = 0;
-    for (; t + 4 <= n_trees; t += 4) {
-      const uint32_t a = __ldg(p + (t + 0) * tree_stride), b = __ldg(p + (t + 1) * tree_stride);
-      const uint32_t d = __ldg(p + (t + 2) * tree_stride), e = __ldg(p + (t + 3) * tree_stride);
-      c += ((a >> lane) & 1u) + ((b >> lane) & 1u) + ((d >> lane) & 1u) + ((e >> lane) & 1u);
-    }
-    for (; t < n_trees; ++t) c += (__ldg(p + t * tree_stride) >> lane) & 1u;
-    if (counts) counts[wi * 32 + lane] = c;
-    if (out) {
-      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, int64_t(c) >= k_min);
-      if (lane == 0) out[wi] = bal;
+// One thread per (region, pyramid word).  Per-bit tree counts are kept as
+// SWAR byte counters (acc[q] byte j counts bit q + 8j: 16 ops per tree and
+// word), folded into 32-bit counters every 255 trees.  Loads are coalesced
+// across threads (consecutive words of one tree).
+
+// Merged leaf word m (path-code order) -> OR its 32 bits into the cube-order
+// classify operand: the inverse of morton_word_from_cube (8 nibbles).
+__device__ __forceinline__ void scatter_leaf_word_to_cube(uint32_t word, uint32_t m, int L, uint32_t* cube) {
+  if (!word) return;
+  if (L == 1) { atomicOr(cube, word & 0xFFu); return; }
+  const uint32_t base = code_to_cube(m << 5, L);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const uint32_t g0 = c & 1, r0 = (c >> 1) & 1, g1 = (c >> 2) & 1;
+    const int off = g0 * 2 + r0 * 4 + g1 * 16;
+    const uint32_t nib = ((word >> off) & 3u) | (((word >> (off + 8)) & 3u) << 2);
+    if (nib) {
+      const uint32_t idx = base + ((g0 | (g1 << 1)) << L) + (r0 << (2 * L));
+      atomicOr(cube + (idx >> 5), nib << (idx & 31u));
     }
   }
 }
 
+__device__ __forceinline__ void finish_word(const uint32_t (&c32)[32], int64_t wi, int64_t w, int64_t r,
+                                            int64_t k_min, int L, int64_t leaf_off, int64_t CW,
+                                            uint32_t* counts, uint32_t* out, uint32_t* cube) {
+  if (counts) {
+    uint4* dst = reinterpret_cast<uint4*>(counts + wi * 32);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) dst[q] = make_uint4(c32[4 * q], c32[4 * q + 1], c32[4 * q + 2], c32[4 * q + 3]);
+  }
+  if (out) {
+    uint32_t bits = 0;
+#pragma unroll
+    for (int b = 0; b < 32; ++b) bits |= uint32_t(int64_t(c32[b]) >= k_min) << b;
+    out[wi] = bits;
+    if (cube && w >= leaf_off) scatter_leaf_word_to_cube(bits, uint32_t(w - leaf_off), L, cube + r * CW);
+  }
+}
+
 __global__ void __launch_bounds__(256)
-k_threshold(const uint32_t* __restrict__ counts, int64_t total_words, int64_t k_min, uint32_t* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t n_warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t wi = warp; wi < total_words; wi += n_warps) {
-    const uint32_t c = counts[wi * 32 + lane];
-    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, int64_t(c) >= k_min);
-    if (lane == 0) out[wi] = bal;
+k_merge(const uint32_t* __restrict__ pyr, int n_trees, int n_regions, int L, int64_t k_min,
+        uint32_t* __restrict__ counts, uint32_t* __restrict__ out, uint32_t* __restrict__ cube) {
+  const int64_t PW = pyr_words(L);
+  const int64_t total = PW * n_regions;
+  const int64_t leaf_off = level_offset(L), CW = cube_words(L);
+  for (int64_t wi = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; wi < total;
+       wi += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = wi / PW, w = wi - r * PW;
+    const uint32_t* p = pyr + wi;               // tree t at p + t * total
+    uint32_t c32[32];
+#pragma unroll
+    for (int b = 0; b < 32; ++b) c32[b] = 0;
+    for (int t0 = 0; t0 < n_trees; t0 += 255) {
+      const int t1 = min(n_trees, t0 + 255);
+      uint32_t acc[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = 0;
+      int t = t0;
+      for (; t + 4 <= t1; t += 4) {
+        const uint32_t a = __ldg(p + (t + 0) * total), b = __ldg(p + (t + 1) * total);
+        const uint32_t d = __ldg(p + (t + 2) * total), e = __ldg(p + (t + 3) * total);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          acc[q] += ((a >> q) & 0x01010101u) + ((b >> q) & 0x01010101u) + ((d >> q) & 0x01010101u) +
+                    ((e >> q) & 0x01010101u);
+      }
+      for (; t < t1; ++t) {
+        const uint32_t a = __ldg(p + t * total);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] += (a >> q) & 0x01010101u;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c32[q + 8 * j] += (acc[q] >> (8 * j)) & 0xFFu;
+      }
+    }
+    finish_word(c32, wi, w, r, k_min, L, leaf_off, CW, counts, out, cube);
+  }
+}
+
+__global__ void __launch_bounds__(256)
+k_threshold(const uint32_t* __restrict__ counts, int n_regions, int L, int64_t k_min, uint32_t* __restrict__ out,
+            uint32_t* __restrict__ cube) {
+  const int64_t PW = pyr_words(L);
+  const int64_t total = PW * n_regions;
+  const int64_t leaf_off = level_offset(L), CW = cube_words(L);
+  for (int64_t wi = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; wi < total;
+       wi += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = wi / PW, w = wi - r * PW;
+    uint32_t c32[32];
+    const uint4* src = reinterpret_cast<const uint4*>(counts + wi * 32);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint4 v = src[q];
+      c32[4 * q] = v.x; c32[4 * q + 1] = v.y; c32[4 * q + 2] = v.z; c32[4 * q + 3] = v.w;
+    }
+    finish_word(c32, wi, w, r, k_min, L, leaf_off, CW, nullptr, out, cube);
   }
 }
 
@@ -458,7 +537,7 @@ k_classify_flat(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_p
   constexpr int64_t CW = cube_words(L);
   const uint32_t* bits = cube;
   if constexpr (SMEM_BITS) {
-    for (int i = threadIdx.x; i < CW; i += CLS_BLOCK) s_bits[i] = __ldg(cube + i);
+    for (int i = threadIdx.x; i < CW; i += CLS_BLOCK) s_bits[Swz<L>::word(i)] = __ldg(cube + i);
     __syncthreads();
     bits = s_bits;
   }
@@ -466,22 +545,25 @@ k_classify_flat(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_p
   for (int64_t u = int64_t(blockIdx.x) * CLS_BLOCK + threadIdx.x; u < n_units; u += stride) {
     uint32_t w[12];
     load_unit(frames, u, w);
-    uint32_t idx[16];
-    idx[0] = cube_idx<L>(pixel_word<0>(w));   idx[1] = cube_idx<L>(pixel_word<1>(w));
-    idx[2] = cube_idx<L>(pixel_word<2>(w));   idx[3] = cube_idx<L>(pixel_word<3>(w));
-    idx[4] = cube_idx<L>(pixel_word<4>(w));   idx[5] = cube_idx<L>(pixel_word<5>(w));
-    idx[6] = cube_idx<L>(pixel_word<6>(w));   idx[7] = cube_idx<L>(pixel_word<7>(w));
-    idx[8] = cube_idx<L>(pixel_word<8>(w));   idx[9] = cube_idx<L>(pixel_word<9>(w));
-    idx[10] = cube_idx<L>(pixel_word<10>(w)); idx[11] = cube_idx<L>(pixel_word<11>(w));
-    idx[12] = cube_idx<L>(pixel_word<12>(w)); idx[13] = cube_idx<L>(pixel_word<13>(w));
-    idx[14] = cube_idx<L>(pixel_word<14>(w)); idx[15] = cube_idx<L>(pixel_word<15>(w));
+    uint32_t px[16];
+    px[0] = pixel_word<0>(w);   px[1] = pixel_word<1>(w);   px[2] = pixel_word<2>(w);
+    px[3] = pixel_word<3>(w);   px[4] = pixel_word<4>(w);   px[5] = pixel_word<5>(w);
+    px[6] = pixel_word<6>(w);   px[7] = pixel_word<7>(w);   px[8] = pixel_word<8>(w);
+    px[9] = pixel_word<9>(w);   px[10] = pixel_word<10>(w); px[11] = pixel_word<11>(w);
+    px[12] = pixel_word<12>(w); px[13] = pixel_word<13>(w); px[14] = pixel_word<14>(w);
+    px[15] = pixel_word<15>(w);
     uint32_t v[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
+      uint32_t idx = cube_idx<L>(px[j]);
       uint32_t wd;
-      if constexpr (SMEM_BITS) wd = bits[idx[j] >> 5];
-      else wd = __ldg(bits + (idx[j] >> 5));
-      v[j] = __funnelshift_r(wd, wd, idx[j]);      // bit 0 = background
+      if constexpr (SMEM_BITS) {
+        idx = swizzle_idx<L>(idx, px[j]);
+        wd = bits[idx >> 5];
+      } else {
+        wd = __ldg(bits + (idx >> 5));
+      }
+      v[j] = __funnelshift_r(wd, wd, idx);      // bit 0 = background
     }
     if constexpr (!PACKED) {
       uint4 o;
@@ -503,7 +585,8 @@ k_classify_flat(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_p
   if constexpr (!PACKED) {
     if (blockIdx.x == 0) {
       for (int64_t i = n_units * 16 + threadIdx.x; i < n_pixels; i += CLS_BLOCK) {
-        const uint32_t idx = cube_idx<L>(rgb_word_scalar(frames + 3 * i));
+        const uint32_t x = rgb_word_scalar(frames + 3 * i);
+        const uint32_t idx = SMEM_BITS ? swizzle_idx<L>(cube_idx<L>(x), x) : cube_idx<L>(x);
         const uint32_t wd = SMEM_BITS ? bits[idx >> 5] : __ldg(bits + (idx >> 5));
         mask[i] = uint8_t(((wd >> (idx & 31u)) & 1u) ^ 1u);
       }
@@ -789,15 +872,16 @@ int obg_prune(const uint32_t* pyramids, int n_trees, int levels, int new_levels,
 }
 
 static int merge_common(const uint32_t* pyramids, int n_trees, int n_regions, int levels, int64_t k_min,
-                        uint32_t* counts, uint32_t* out, void* stream) {
+                        uint32_t* counts, uint32_t* out, uint32_t* out_cube, void* stream) {
   if (levels < 1 || levels > 8) return set_err(OBG_EINVAL, "levels must be in 1..8, got %d", levels);
   if (n_trees < 1) return set_err(OBG_EINVAL, "no trees to merge");
   if (n_regions < 1) return set_err(OBG_EINVAL, "n_regions must be >= 1");
   if (!pyramids) return set_err(OBG_EINVAL, "null buffer");
-  const int64_t PW = pyr_words(levels);
-  const int64_t warps = PW * n_regions;
-  k_merge<<<grid_for(warps * 32, 256, sm_count() * 8), 256, 0, as_stream(stream)>>>(pyramids, n_trees, n_regions, PW,
-                                                                                    k_min, counts, out);
+  cudaStream_t st = as_stream(stream);
+  if (out_cube) CUDA_TRY(cudaMemsetAsync(out_cube, 0, size_t(n_regions) * cube_words(levels) * 4, st));
+  const int64_t words = pyr_words(levels) * n_regions;
+  k_merge<<<grid_for(words, 256, sm_count() * 8), 256, 0, st>>>(pyramids, n_trees, n_regions, levels, k_min,
+                                                               counts, out, out_cube);
   LAUNCH_CHECK("k_merge");
   return OBG_OK;
 }
@@ -805,27 +889,29 @@ static int merge_common(const uint32_t* pyramids, int n_trees, int n_regions, in
 int obg_merge_counts(const uint32_t* pyramids, int n_trees, int n_regions, int levels, uint32_t* counts, void* stream) {
   g_err[0] = 0;
   if (!counts) return set_err(OBG_EINVAL, "null buffer");
-  return merge_common(pyramids, n_trees, n_regions, levels, 0, counts, nullptr, stream);
+  return merge_common(pyramids, n_trees, n_regions, levels, 0, counts, nullptr, nullptr, stream);
 }
 
 int obg_merge(const uint32_t* pyramids, int n_trees, int n_regions, int levels, int64_t k_min,
-              uint32_t* out_pyramids, void* stream) {
+              uint32_t* out_pyramids, uint32_t* out_cube, void* stream) {
   g_err[0] = 0;
   if (!out_pyramids) return set_err(OBG_EINVAL, "null buffer");
   if (k_min < 1) return set_err(OBG_EINVAL, "k_min must be >= 1, got %lld", (long long)k_min);
-  return merge_common(pyramids, n_trees, n_regions, levels, k_min, nullptr, out_pyramids, stream);
+  return merge_common(pyramids, n_trees, n_regions, levels, k_min, nullptr, out_pyramids, out_cube, stream);
 }
 
 int obg_merge_threshold(const uint32_t* counts, int n_regions, int levels, int64_t k_min, uint32_t* out_pyramids,
-                        void* stream) {
+                        uint32_t* out_cube, void* stream) {
   g_err[0] = 0;
   if (levels < 1 || levels > 8) return set_err(OBG_EINVAL, "levels must be in 1..8, got %d", levels);
   if (n_regions < 1) return set_err(OBG_EINVAL, "n_regions must be >= 1");
   if (k_min < 1) return set_err(OBG_EINVAL, "k_min must be >= 1, got %lld", (long long)k_min);
   if (!counts || !out_pyramids) return set_err(OBG_EINVAL, "null buffer");
+  cudaStream_t st = as_stream(stream);
+  if (out_cube) CUDA_TRY(cudaMemsetAsync(out_cube, 0, size_t(n_regions) * cube_words(levels) * 4, st));
   const int64_t words = pyr_words(levels) * n_regions;
-  k_threshold<<<grid_for(words * 32, 256, sm_count() * 8), 256, 0, as_stream(stream)>>>(counts, words, k_min,
-                                                                                        out_pyramids);
+  k_threshold<<<grid_for(words, 256, sm_count() * 8), 256, 0, st>>>(counts, n_regions, levels, k_min,
+                                                                   out_pyramids, out_cube);
   LAUNCH_CHECK("k_threshold");
   return OBG_OK;
 }

@@ -63,9 +63,8 @@ def build_background_model_sharded(frames_dev, config: ModelConfig, group=None, 
         total = global_trees
     k_min = merge_k_min(total, config.threshold)
     merged = _device.empty((n_regions, pw), "int32")
-    _lib.check(lib.obg_merge_threshold(_device.ptr(counts), n_regions, L, k_min, _device.ptr(merged),
-                                       _device.stream_handle()))
     cube = _device.empty((n_regions, _lib.cube_words(L)), "int32")
-    _lib.check(lib.obg_leaf_cube(_device.ptr(merged), n_regions, L, _device.ptr(cube), _device.stream_handle()))
+    _lib.check(lib.obg_merge_threshold(_device.ptr(counts), n_regions, L, k_min, _device.ptr(merged),
+                                       _device.ptr(cube), _device.stream_handle()))
     return BackgroundModel(config, frame_width=w, frame_height=h, _device_pyramids=merged, _device_cube=cube)
 

@@ -211,15 +211,17 @@ def build_presence(frames_dev, levels: int, grid_rows: int = 1, grid_cols: int =
     return (out, cnt) if counts else out
 
 
-def merge_pyramids(pyramids_dev, levels: int, k_min: int):
-    """GPU merge: ``[n_trees, R*C, PW]`` -> merged ``[R*C, PW]``."""
+def merge_pyramids(pyramids_dev, levels: int, k_min: int, with_cube: bool = False):
+    """GPU merge: ``[n_trees, R*C, PW]`` -> merged ``[R*C, PW]`` (and, with
+    ``with_cube``, the merged leaves in cube order ``[R*C, CW]`` for classify)."""
     from . import _device
     n_trees, n_regions = int(pyramids_dev.shape[0]), int(pyramids_dev.shape[1])
     out = _device.empty((n_regions, _lib.pyramid_words(levels)), "int32")
+    cube = _device.empty((n_regions, _lib.cube_words(levels)), "int32") if with_cube else None
     lib = _lib.load()
     _lib.check(lib.obg_merge(_device.ptr(pyramids_dev), n_trees, n_regions, levels, k_min, _device.ptr(out),
-                             _device.stream_handle()))
-    return out
+                             _device.ptr(cube) if with_cube else None, _device.stream_handle()))
+    return (out, cube) if with_cube else out
 
 
 def build_frame_tree(frames, region: tuple[int, int], config: ModelConfig) -> Octree:
@@ -294,12 +296,7 @@ def build_background_model_device(frames_dev, config: ModelConfig, n_groups: int
             raise ValueError(f"need at least {config.group_size} frames for one group, got {n}")
         frames_dev = frames_dev[: n_groups * config.group_size]
     pyr = build_presence(frames_dev, config.levels, config.grid_rows, config.grid_cols, config.group_size)
-    merged = merge_pyramids(pyr, config.levels, merge_k_min(n_groups, config.threshold))
-    n_regions = config.grid_rows * config.grid_cols
-    cube = _device.empty((n_regions, _lib.cube_words(config.levels)), "int32")
-    lib = _lib.load()
-    _lib.check(lib.obg_leaf_cube(_device.ptr(merged), n_regions, config.levels, _device.ptr(cube),
-                                 _device.stream_handle()))
+    merged, cube = merge_pyramids(pyr, config.levels, merge_k_min(n_groups, config.threshold), with_cube=True)
     return BackgroundModel(config, frame_width=w, frame_height=h, _device_pyramids=merged, _device_cube=cube)
 
 

@@ -48,8 +48,8 @@ def test_size_helpers():
     lambda lib: lib.obg_build_presence(None, 2, 8, 8, 4, 1, 1, 3, None, None, None, 0, None),
     lambda lib: lib.obg_classify(None, 1, 8, 8, 4, 0, 1, None, None, 0, None),
     lambda lib: lib.obg_classify(None, 1, 8, 8, 4, 1, 1, None, None, 7, None),
-    lambda lib: lib.obg_merge(None, 0, 1, 4, 1, None, None),
-    lambda lib: lib.obg_merge(None, 2, 1, 4, 0, None, None),
+    lambda lib: lib.obg_merge(None, 0, 1, 4, 1, None, None, None),
+    lambda lib: lib.obg_merge(None, 2, 1, 4, 0, None, None, None),
     lambda lib: lib.obg_prune(None, 1, 3, 4, None, None),
     lambda lib: lib.obg_pack_codes(None, 5, 0, None, None),
 ])

@@ -280,9 +280,32 @@ def test_merge_counts_and_threshold(cuda):
     pw = _lib.pyramid_words(levels)
     counts = _device.empty((1, pw * 32), "int32")
     _lib.check(lib.obg_merge_counts(_device.ptr(pyr), n, 1, levels, _device.ptr(counts), _device.stream_handle()))
+    want_counts = sum(np.unpackbits(t._host().view(np.uint8), bitorder="little").astype(np.int64) for t in trees)
+    assert np.array_equal(counts.cpu().numpy()[0], want_counts)
     for k_min in (1, 3, 6, 11):
         out = _device.empty((1, pw), "int32")
+        cube = _device.empty((1, _lib.cube_words(levels)), "int32")
         _lib.check(lib.obg_merge_threshold(_device.ptr(counts), 1, levels, k_min, _device.ptr(out),
-                                           _device.stream_handle()))
-        fused = obg.merge_pyramids(pyr, levels, k_min)
-        assert cuda.equal(out, fused)
+                                           _device.ptr(cube), _device.stream_handle()))
+        fused, fused_cube = obg.merge_pyramids(pyr, levels, k_min, with_cube=True)
+        assert cuda.equal(out, fused) and cuda.equal(cube, fused_cube)
+        ref_cube = _device.empty((1, _lib.cube_words(levels)), "int32")
+        _lib.check(lib.obg_leaf_cube(_device.ptr(out), 1, levels, _device.ptr(ref_cube), _device.stream_handle()))
+        assert cuda.equal(cube, ref_cube)
+
+
+@pytest.mark.parametrize("levels", range(1, 9))
+def test_fused_merge_cube_matches_leaf_cube(cuda, levels):
+    from paper_1412_1945_b200 import _device
+    lib = _lib.load()
+    rng = np.random.default_rng(levels + 40)
+    trees = [orc.tree_from_codes(rng.integers(0, 8 ** levels, size=int(rng.integers(1, 3000))), levels)
+             for _ in range(7)]
+    pyr = cuda.stack([Octree.from_bytes(orc.to_bytes(t), levels)._device() for t in trees]).unsqueeze(1)
+    for k_min in (1, 2, 4, 7):
+        merged, cube = obg.merge_pyramids(pyr.contiguous(), levels, k_min, with_cube=True)
+        ref_cube = _device.empty((1, _lib.cube_words(levels)), "int32")
+        _lib.check(lib.obg_leaf_cube(_device.ptr(merged), 1, levels, _device.ptr(ref_cube), _device.stream_handle()))
+        assert cuda.equal(cube, ref_cube)
+        want = orc.merge_trees(trees, k_min / 7 - 1e-12, levels)
+        assert Octree._from_device(merged[0], levels).to_bytes() == orc.to_bytes(want)
