@@ -285,7 +285,7 @@ k_build_generic(const uint8_t* __restrict__ frames, int64_t n_pixels_used, int H
 //     per-level pyramids.  One CTA per (tree, chunk of <= 1024 leaf words).
 // ===========================================================================
 constexpr int PYR_BLOCK = 256;
-constexpr int PYR_CHUNK = 256;   // leaf-level words per CTA
+constexpr int PYR_CHUNK = 1024;  // leaf-level words per CTA (a 32x32x32 sub-cube)
 
 // Leaf-level path-order word m (codes 32m..32m+31) from a cube bitset.
 // Codes of one word share all but bits 0..4 = b0 g0 r0 b1 g1; the (b1,b0)
@@ -318,6 +318,7 @@ template <bool FROM_CUBE>
 __global__ void __launch_bounds__(PYR_BLOCK)
 k_pyramid(const uint32_t* __restrict__ src, int64_t src_stride, int L, uint32_t* __restrict__ out) {
   __shared__ uint32_t s_w[PYR_CHUNK];
+  __shared__ uint32_t s_c[PYR_CHUNK];
   const int64_t tree = blockIdx.y;
   const int64_t LW = level_words(L);
   const int64_t PW = pyr_words(L);
@@ -326,13 +327,39 @@ k_pyramid(const uint32_t* __restrict__ src, int64_t src_stride, int L, uint32_t*
   const uint32_t* s = src + tree * src_stride;
   uint32_t* o = out + tree * PW;
   // leaf level
-  for (int i = threadIdx.x; i < nw; i += PYR_BLOCK) {
-    uint32_t x;
-    if constexpr (FROM_CUBE) x = morton_word_from_cube(s, uint32_t(w0 + i), L);
-    else x = s[w0 + i];
-    if (L == 1) x &= 0xFFu;
-    s_w[i] = x;
-    if (x) o[level_offset(L) + w0 + i] = x;   // the chunk owns these words
+  if (FROM_CUBE && L >= 5) {
+    // The chunk is the level-(L-5) node w0/1024: a 32x32x32 sub-cube whose
+    // 1024 (R', G') rows are one cube word each.  Stage them, then gather.
+    const uint32_t cb = code_to_cube(uint32_t(w0) << 5, L);
+    const uint32_t M = (1u << L) - 1u;
+    const uint32_t Rb = (cb >> (2 * L)) & M, Gb = (cb >> L) & M, Bw = (cb & M) >> 5;
+    for (int t = threadIdx.x; t < PYR_CHUNK; t += PYR_BLOCK) {
+      const uint32_t r = t >> 5, g = t & 31;
+      s_c[t] = s[(int64_t(Rb + r) << (2 * L - 5)) | (int64_t(Gb + g) << (L - 5)) | Bw];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < PYR_CHUNK; i += PYR_BLOCK) {
+      const uint32_t c = uint32_t(i) << 5;
+      const uint32_t rl = compact3(c >> 2), gl = compact3(c >> 1), bl = compact3(c);
+      uint32_t x = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t g0 = k & 1, r0 = (k >> 1) & 1, g1 = (k >> 2) & 1;
+        const uint32_t nib = (s_c[((rl + r0) << 5) + gl + g0 + 2 * g1] >> bl) & 0xFu;
+        x |= ((nib & 3u) | ((nib & 12u) << 6)) << (g0 * 2 + r0 * 4 + g1 * 16);
+      }
+      s_w[i] = x;
+      if (x) o[level_offset(L) + w0 + i] = x;
+    }
+  } else {
+    for (int i = threadIdx.x; i < nw; i += PYR_BLOCK) {
+      uint32_t x;
+      if constexpr (FROM_CUBE) x = morton_word_from_cube(s, uint32_t(w0 + i), L);
+      else x = s[w0 + i];
+      if (L == 1) x &= 0xFFu;
+      s_w[i] = x;
+      if (x) o[level_offset(L) + w0 + i] = x;   // the chunk owns these words
+    }
   }
   __syncthreads();
   // bit range of the chunk at the current level: [B, B + n)
@@ -429,45 +456,95 @@ __device__ __forceinline__ void finish_word(const uint32_t (&c32)[32], int64_t w
   }
 }
 
-__global__ void __launch_bounds__(256)
+// Block = 32 words (threadIdx.x, coalesced loads) x 8 tree groups
+// (threadIdx.y): thread (x, y) counts trees y, y+8, ... of word x with SWAR
+// byte counters, so each thread keeps <= ceil(n/8) independent loads in
+// flight.  Groups are combined in shared memory; more than 255 trees per
+// thread spill into 32-bit shared counters.
+constexpr int MERGE_GROUPS = 8;
+__global__ void __launch_bounds__(32 * MERGE_GROUPS)
 k_merge(const uint32_t* __restrict__ pyr, int n_trees, int n_regions, int L, int64_t k_min,
         uint32_t* __restrict__ counts, uint32_t* __restrict__ out, uint32_t* __restrict__ cube) {
+  __shared__ uint32_t s_acc[MERGE_GROUPS][8][32];
+  __shared__ uint32_t s_wide[32][33];
+  __shared__ uint32_t s_bits[MERGE_GROUPS][32];
+  const int x = threadIdx.x, y = threadIdx.y;
   const int64_t PW = pyr_words(L);
   const int64_t total = PW * n_regions;
   const int64_t leaf_off = level_offset(L), CW = cube_words(L);
-  for (int64_t wi = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; wi < total;
-       wi += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t r = wi / PW, w = wi - r * PW;
-    const uint32_t* p = pyr + wi;               // tree t at p + t * total
-    uint32_t c32[32];
+  const bool wide = (n_trees + MERGE_GROUPS - 1) / MERGE_GROUPS >= 252;   // a thread may flush
+  for (int64_t base = int64_t(blockIdx.x) * 32; base < total; base += int64_t(gridDim.x) * 32) {
+    const int64_t wi = base + x;
+    const bool valid = wi < total;
+    if (wide) {
+      for (int i = y * 32 + x; i < 32 * 33; i += 32 * MERGE_GROUPS) (&s_wide[0][0])[i] = 0;
+      __syncthreads();
+    }
+    uint32_t acc[8];
 #pragma unroll
-    for (int b = 0; b < 32; ++b) c32[b] = 0;
-    for (int t0 = 0; t0 < n_trees; t0 += 255) {
-      const int t1 = min(n_trees, t0 + 255);
-      uint32_t acc[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) acc[q] = 0;
-      int t = t0;
-      for (; t + 4 <= t1; t += 4) {
-        const uint32_t a = __ldg(p + (t + 0) * total), b = __ldg(p + (t + 1) * total);
-        const uint32_t d = __ldg(p + (t + 2) * total), e = __ldg(p + (t + 3) * total);
+    for (int q = 0; q < 8; ++q) acc[q] = 0;
+    int since = 0;
+    if (valid) {
+      const uint32_t* p = pyr + wi;
+      int t = y;
+      for (; t + 3 * MERGE_GROUPS < n_trees; t += 4 * MERGE_GROUPS) {
+        const uint32_t a = __ldg(p + int64_t(t) * total), b = __ldg(p + int64_t(t + MERGE_GROUPS) * total);
+        const uint32_t d = __ldg(p + int64_t(t + 2 * MERGE_GROUPS) * total);
+        const uint32_t e = __ldg(p + int64_t(t + 3 * MERGE_GROUPS) * total);
 #pragma unroll
         for (int q = 0; q < 8; ++q)
           acc[q] += ((a >> q) & 0x01010101u) + ((b >> q) & 0x01010101u) + ((d >> q) & 0x01010101u) +
                     ((e >> q) & 0x01010101u);
+        since += 4;
+        if (since > 251) {   // keep byte counters below 256
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) atomicAdd(&s_wide[x][q + 8 * j], (acc[q] >> (8 * j)) & 0xFFu);
+            acc[q] = 0;
+          }
+          since = 0;
+        }
       }
-      for (; t < t1; ++t) {
-        const uint32_t a = __ldg(p + t * total);
+      for (; t < n_trees; t += MERGE_GROUPS) {
+        const uint32_t a = __ldg(p + int64_t(t) * total);
 #pragma unroll
         for (int q = 0; q < 8; ++q) acc[q] += (a >> q) & 0x01010101u;
       }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) c32[q + 8 * j] += (acc[q] >> (8 * j)) & 0xFFu;
-      }
     }
-    finish_word(c32, wi, w, r, k_min, L, leaf_off, CW, counts, out, cube);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s_acc[y][q][x] = acc[q];
+    __syncthreads();
+    // thread (x, y) totals bits y, y+8, y+16, y+24 of word x
+    uint32_t c[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int g = 0; g < MERGE_GROUPS; ++g) {
+      const uint32_t v = s_acc[g][y][x];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) c[j] += (v >> (8 * j)) & 0xFFu;
+    }
+    if (wide) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) c[j] += s_wide[x][y + 8 * j];
+    }
+    uint32_t part = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) part |= uint32_t(int64_t(c[j]) >= k_min) << (y + 8 * j);
+    s_bits[y][x] = part;
+    if (valid && counts) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) counts[wi * 32 + y + 8 * j] = c[j];
+    }
+    __syncthreads();
+    if (y == 0 && valid && out) {
+      uint32_t bits = 0;
+#pragma unroll
+      for (int g = 0; g < MERGE_GROUPS; ++g) bits |= s_bits[g][x];
+      out[wi] = bits;
+      const int64_t r = wi / PW, w = wi - r * PW;
+      if (cube && w >= leaf_off) scatter_leaf_word_to_cube(bits, uint32_t(w - leaf_off), L, cube + r * CW);
+    }
+    __syncthreads();
   }
 }
 
@@ -880,8 +957,8 @@ static int merge_common(const uint32_t* pyramids, int n_trees, int n_regions, in
   cudaStream_t st = as_stream(stream);
   if (out_cube) CUDA_TRY(cudaMemsetAsync(out_cube, 0, size_t(n_regions) * cube_words(levels) * 4, st));
   const int64_t words = pyr_words(levels) * n_regions;
-  k_merge<<<grid_for(words, 256, sm_count() * 8), 256, 0, st>>>(pyramids, n_trees, n_regions, levels, k_min,
-                                                               counts, out, out_cube);
+  k_merge<<<grid_for(words, 32, sm_count() * 16), dim3(32, MERGE_GROUPS), 0, st>>>(
+      pyramids, n_trees, n_regions, levels, k_min, counts, out, out_cube);
   LAUNCH_CHECK("k_merge");
   return OBG_OK;
 }

@@ -309,3 +309,17 @@ def test_fused_merge_cube_matches_leaf_cube(cuda, levels):
         assert cuda.equal(cube, ref_cube)
         want = orc.merge_trees(trees, k_min / 7 - 1e-12, levels)
         assert Octree._from_device(merged[0], levels).to_bytes() == orc.to_bytes(want)
+
+
+@pytest.mark.parametrize("n_trees", [1, 7, 8, 9, 255, 2015, 2017, 2100])
+def test_merge_many_trees(cuda, n_trees):
+    """SWAR byte counters and their 32-bit spill path (> 2016 trees)."""
+    rng = np.random.default_rng(n_trees)
+    levels = 2
+    trees = [orc.tree_from_codes(rng.integers(0, 64, size=int(rng.integers(0, 12))), levels) for _ in range(n_trees)]
+    pyr = cuda.stack([(Octree.from_bytes(orc.to_bytes(t), levels) if t.root else Octree(levels))._device()
+                      for t in trees]).unsqueeze(1).contiguous()
+    for thr in (1.0 / n_trees, 0.1, 0.19, 0.5, 1.0):
+        merged = obg.merge_pyramids(pyr, levels, obg.merge_k_min(n_trees, thr))
+        want = orc.merge_trees(trees, thr, levels)
+        assert Octree._from_device(merged[0], levels).to_bytes() == orc.to_bytes(want), thr
