@@ -139,12 +139,18 @@ __device__ __forceinline__ uint32_t rgb_word_scalar(const uint8_t* p) {
   return (uint32_t(p[0]) << 8) | (uint32_t(p[1]) << 16) | (uint32_t(p[2]) << 24);
 }
 
+// 48-byte unit = 16 RGB pixels.  volatile asm keeps the three 16-byte loads
+// (and those of a second unit) issued back to back: left to itself ptxas sinks
+// them next to their first use to save registers, which starves the memory
+// pipe (ncu r2: long-scoreboard stalls dominated classify).
 __device__ __forceinline__ void load_unit(const uint8_t* __restrict__ base, int64_t u, uint32_t (&w)[12]) {
-  const uint4* p = reinterpret_cast<const uint4*>(base) + 3 * u;
-  uint4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
-  w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
-  w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
-  w[8] = c.x; w[9] = c.y; w[10] = c.z; w[11] = c.w;
+  const uint8_t* p = base + 48 * u;
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "l"(p));
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4+16];"
+               : "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]) : "l"(p));
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4+32];"
+               : "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]) : "l"(p));
 }
 
 // ---------------------------------------------------------------------------
@@ -198,6 +204,38 @@ __device__ __forceinline__ void count_code(uint32_t* counts, uint32_t idx) {
   if ((threadIdx.x & 31) == leader) atomicAdd(counts + code, (uint32_t)__popc(peers));
 }
 
+// One 16-pixel unit: all lookups first (independent LDS), then the rare
+// check-before-set atomics, so the common path is straight-line code.
+template <int L, bool SMEM_BITS, bool COUNTS>
+__device__ __forceinline__ void build_unit(const uint32_t (&w)[12], uint32_t* bits, uint32_t* cnt) {
+  uint32_t px[16];
+  px[0] = pixel_word<0>(w);   px[1] = pixel_word<1>(w);   px[2] = pixel_word<2>(w);
+  px[3] = pixel_word<3>(w);   px[4] = pixel_word<4>(w);   px[5] = pixel_word<5>(w);
+  px[6] = pixel_word<6>(w);   px[7] = pixel_word<7>(w);   px[8] = pixel_word<8>(w);
+  px[9] = pixel_word<9>(w);   px[10] = pixel_word<10>(w); px[11] = pixel_word<11>(w);
+  px[12] = pixel_word<12>(w); px[13] = pixel_word<13>(w); px[14] = pixel_word<14>(w);
+  px[15] = pixel_word<15>(w);
+#pragma unroll
+  for (int h = 0; h < 16; h += 8) {
+    uint32_t sidx[8], wd[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t idx = cube_idx<L>(px[h + j]);
+      sidx[j] = SMEM_BITS ? swizzle_idx<L>(idx, px[h + j]) : idx;
+      if constexpr (SMEM_BITS) wd[j] = bits[sidx[j] >> 5];
+      else wd[j] = *reinterpret_cast<volatile uint32_t*>(bits + (sidx[j] >> 5));
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (!((wd[j] >> (sidx[j] & 31u)) & 1u)) atomicOr(bits + (sidx[j] >> 5), 1u << (sidx[j] & 31u));
+    }
+  }
+  if constexpr (COUNTS) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) count_code<L>(cnt, cube_idx<L>(px[j]));
+  }
+}
+
 template <int L, bool SMEM_BITS, bool COUNTS>
 __global__ void __launch_bounds__(BUILD_BLOCK)
 k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t total_units,
@@ -221,22 +259,14 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
     if constexpr (SMEM_BITS) bits = s_bits;
     else bits = ws + tree * CW;
     uint32_t* cnt = COUNTS ? counts + tree * (int64_t(1) << (3 * L)) : nullptr;
-    for (int64_t v = u + threadIdx.x; v < seg_end; v += BUILD_BLOCK) {
-      uint32_t w[12];
-      load_unit(frames, v, w);
-      uint32_t px[16];
-      px[0] = pixel_word<0>(w);   px[1] = pixel_word<1>(w);   px[2] = pixel_word<2>(w);
-      px[3] = pixel_word<3>(w);   px[4] = pixel_word<4>(w);   px[5] = pixel_word<5>(w);
-      px[6] = pixel_word<6>(w);   px[7] = pixel_word<7>(w);   px[8] = pixel_word<8>(w);
-      px[9] = pixel_word<9>(w);   px[10] = pixel_word<10>(w); px[11] = pixel_word<11>(w);
-      px[12] = pixel_word<12>(w); px[13] = pixel_word<13>(w); px[14] = pixel_word<14>(w);
-      px[15] = pixel_word<15>(w);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const uint32_t idx = cube_idx<L>(px[j]);
-        set_bit<L, SMEM_BITS>(bits, SMEM_BITS ? swizzle_idx<L>(idx, px[j]) : idx);
-        if constexpr (COUNTS) count_code<L>(cnt, idx);
-      }
+    // two units per thread and iteration: six 16-byte loads in flight
+    for (int64_t v = u + threadIdx.x; v < seg_end; v += 2 * BUILD_BLOCK) {
+      const bool second = v + BUILD_BLOCK < seg_end;
+      uint32_t wa[12], wb[12];
+      load_unit(frames, v, wa);
+      if (second) load_unit(frames, v + BUILD_BLOCK, wb);
+      build_unit<L, SMEM_BITS, COUNTS>(wa, bits, cnt);
+      if (second) build_unit<L, SMEM_BITS, COUNTS>(wb, bits, cnt);
     }
     if constexpr (SMEM_BITS) {
       __syncthreads();
@@ -606,8 +636,49 @@ constexpr int CLS_BLOCK = 256;
 // Flat path: 1x1 grid, leaf cube bitset in shared memory (L <= 6) or read
 // through L1/L2 (L >= 7).  One thread = one 16-pixel unit per iteration:
 // 3 x 16-byte loads, 16 lookups, one 16-byte (u8) or 2-byte (packed) store.
+// One 16-pixel unit -> 16 mask bytes (or 16 mask bits).
 template <int L, bool SMEM_BITS, bool PACKED>
-__global__ void __launch_bounds__(CLS_BLOCK)
+__device__ __forceinline__ void classify_unit(const uint32_t (&w)[12], const uint32_t* bits, uint8_t* mask,
+                                              int64_t u) {
+  uint32_t px[16];
+  px[0] = pixel_word<0>(w);   px[1] = pixel_word<1>(w);   px[2] = pixel_word<2>(w);
+  px[3] = pixel_word<3>(w);   px[4] = pixel_word<4>(w);   px[5] = pixel_word<5>(w);
+  px[6] = pixel_word<6>(w);   px[7] = pixel_word<7>(w);   px[8] = pixel_word<8>(w);
+  px[9] = pixel_word<9>(w);   px[10] = pixel_word<10>(w); px[11] = pixel_word<11>(w);
+  px[12] = pixel_word<12>(w); px[13] = pixel_word<13>(w); px[14] = pixel_word<14>(w);
+  px[15] = pixel_word<15>(w);
+  uint32_t v[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    uint32_t idx = cube_idx<L>(px[j]);
+    uint32_t wd;
+    if constexpr (SMEM_BITS) {
+      idx = swizzle_idx<L>(idx, px[j]);
+      wd = bits[idx >> 5];
+    } else {
+      wd = __ldg(bits + (idx >> 5));
+    }
+    v[j] = __funnelshift_r(wd, wd, idx);      // bit 0 = background
+  }
+  if constexpr (!PACKED) {
+    uint4 o;
+    o.x = __byte_perm(__byte_perm(v[0], v[1], 0x0040), __byte_perm(v[2], v[3], 0x0040), 0x5410);
+    o.y = __byte_perm(__byte_perm(v[4], v[5], 0x0040), __byte_perm(v[6], v[7], 0x0040), 0x5410);
+    o.z = __byte_perm(__byte_perm(v[8], v[9], 0x0040), __byte_perm(v[10], v[11], 0x0040), 0x5410);
+    o.w = __byte_perm(__byte_perm(v[12], v[13], 0x0040), __byte_perm(v[14], v[15], 0x0040), 0x5410);
+    o.x = ~o.x & 0x01010101u; o.y = ~o.y & 0x01010101u;
+    o.z = ~o.z & 0x01010101u; o.w = ~o.w & 0x01010101u;
+    __stcs(reinterpret_cast<uint4*>(mask) + u, o);
+  } else {
+    uint32_t b = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) b |= (v[j] & 1u) << j;
+    reinterpret_cast<uint16_t*>(mask)[u] = uint16_t(~b & 0xFFFFu);
+  }
+}
+
+template <int L, bool SMEM_BITS, bool PACKED>
+__global__ void __launch_bounds__(CLS_BLOCK, 2)
 k_classify_flat(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_pixels,
                 const uint32_t* __restrict__ cube, uint8_t* __restrict__ mask) {
   extern __shared__ uint32_t s_bits[];
@@ -619,44 +690,14 @@ k_classify_flat(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_p
     bits = s_bits;
   }
   const int64_t stride = int64_t(gridDim.x) * CLS_BLOCK;
-  for (int64_t u = int64_t(blockIdx.x) * CLS_BLOCK + threadIdx.x; u < n_units; u += stride) {
-    uint32_t w[12];
-    load_unit(frames, u, w);
-    uint32_t px[16];
-    px[0] = pixel_word<0>(w);   px[1] = pixel_word<1>(w);   px[2] = pixel_word<2>(w);
-    px[3] = pixel_word<3>(w);   px[4] = pixel_word<4>(w);   px[5] = pixel_word<5>(w);
-    px[6] = pixel_word<6>(w);   px[7] = pixel_word<7>(w);   px[8] = pixel_word<8>(w);
-    px[9] = pixel_word<9>(w);   px[10] = pixel_word<10>(w); px[11] = pixel_word<11>(w);
-    px[12] = pixel_word<12>(w); px[13] = pixel_word<13>(w); px[14] = pixel_word<14>(w);
-    px[15] = pixel_word<15>(w);
-    uint32_t v[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      uint32_t idx = cube_idx<L>(px[j]);
-      uint32_t wd;
-      if constexpr (SMEM_BITS) {
-        idx = swizzle_idx<L>(idx, px[j]);
-        wd = bits[idx >> 5];
-      } else {
-        wd = __ldg(bits + (idx >> 5));
-      }
-      v[j] = __funnelshift_r(wd, wd, idx);      // bit 0 = background
-    }
-    if constexpr (!PACKED) {
-      uint4 o;
-      o.x = __byte_perm(__byte_perm(v[0], v[1], 0x0040), __byte_perm(v[2], v[3], 0x0040), 0x5410);
-      o.y = __byte_perm(__byte_perm(v[4], v[5], 0x0040), __byte_perm(v[6], v[7], 0x0040), 0x5410);
-      o.z = __byte_perm(__byte_perm(v[8], v[9], 0x0040), __byte_perm(v[10], v[11], 0x0040), 0x5410);
-      o.w = __byte_perm(__byte_perm(v[12], v[13], 0x0040), __byte_perm(v[14], v[15], 0x0040), 0x5410);
-      o.x = ~o.x & 0x01010101u; o.y = ~o.y & 0x01010101u;
-      o.z = ~o.z & 0x01010101u; o.w = ~o.w & 0x01010101u;
-      __stcs(reinterpret_cast<uint4*>(mask) + u, o);
-    } else {
-      uint32_t b = 0;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) b |= (v[j] & 1u) << j;
-      reinterpret_cast<uint16_t*>(mask)[u] = uint16_t(~b & 0xFFFFu);
-    }
+  // two units per thread and iteration: six 16-byte loads in flight
+  for (int64_t u = int64_t(blockIdx.x) * CLS_BLOCK + threadIdx.x; u < n_units; u += 2 * stride) {
+    const bool second = u + stride < n_units;
+    uint32_t wa[12], wb[12];
+    load_unit(frames, u, wa);
+    if (second) load_unit(frames, u + stride, wb);
+    classify_unit<L, SMEM_BITS, PACKED>(wa, bits, mask, u);
+    if (second) classify_unit<L, SMEM_BITS, PACKED>(wb, bits, mask, u + stride);
   }
   // tail pixels (n_pixels not a multiple of 16; u8 layout only)
   if constexpr (!PACKED) {
