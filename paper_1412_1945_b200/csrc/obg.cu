@@ -107,23 +107,43 @@ __device__ __forceinline__ uint32_t cube_idx(uint32_t x) {
   return c1 | c2 | c3;
 }
 
-// Shared-memory bank swizzle of the cube bitset (L = 5, 6).  Word w of the
-// cube holds R'<<(2L-5) | G'<<(L-5) | B'>>5; without a swizzle every R' value
-// lands in the same bank, and a warp reading a colour gradient serialises
-// (ncu r1: 6.6x the ideal shared wavefronts).  phys(w) = w ^ (R' & 31) is an
-// involution that spreads R' over the banks; G' and B'>>5 already vary them.
+// Shared-memory layout of the leaf bitset used by the streaming kernels.
+//
+// L = 5, 6 ("skewed rows"): row R' holds the 2^(2L-5) words (G', B'>>5) of
+// the cube plus one pad word, so consecutive R' rows start one bank apart.
+// Without the skew every R' value of a warp lands in the same bank and a
+// warp reading a colour gradient serialises (ncu r1: 6.6x the ideal shared
+// wavefronts).  A pixel's byte address and bit are computed from
+// x = [*, G, B, R] with multiply-high shifts (FMA pipe) so that the ALU pipe,
+// which bounds these kernels (ncu r3: 85 % busy), only sees the masks:
+//   A   = R' * 4*ROWW + G' << (L-3) | (B' >> 5) << 2
+//   bit = B' & 31
+// Other L: the canonical cube words (idx = R'<<2L | G'<<L | B').
 template <int L>
-struct Swz {
-  static constexpr bool on = (L == 5 || L == 6);
-  __host__ __device__ static constexpr uint32_t word(uint32_t w) {
-    return on ? (w ^ ((w >> (2 * L - 5)) & 31u)) : w;
+struct Smem {
+  static constexpr bool skew = (L == 5 || L == 6);
+  static constexpr uint32_t ROWW = skew ? (1u << (2 * L - 5)) + 1u : 1u;   // words per row incl. pad
+  static constexpr int64_t words = skew ? (int64_t(1) << L) * ROWW : cube_words(L);
+  // canonical cube word -> shared word
+  __host__ __device__ static constexpr uint32_t phys(uint32_t w) { return skew ? w + (w >> (2 * L - 5)) : w; }
+  // shared word -> canonical cube word, 0xFFFFFFFF for a pad word
+  __device__ static uint32_t canon(uint32_t p) {
+    if constexpr (!skew) return p;
+    const uint32_t r = p / ROWW, c = p - r * ROWW;
+    return c == ROWW - 1 ? 0xFFFFFFFFu : r * (ROWW - 1) + c;
   }
 };
-// same swizzle applied to a bit index computed from x = [*, R, G, B]
+
+// Skewed-layout byte address and bit selector of pixel x = [*, G, B, R].
 template <int L>
-__device__ __forceinline__ uint32_t swizzle_idx(uint32_t idx, uint32_t x) {
-  if constexpr (Swz<L>::on) return idx ^ ((x >> (11 - L)) & 0x3E0u);
-  else return idx;
+__device__ __forceinline__ void skew_lookup(uint32_t x, uint32_t& addr, uint32_t& bsel) {
+  constexpr int s = 8 - L;
+  const uint32_t r = __umulhi(x, 1u << (8 - s));                    // x >> (24+s) = R'
+  bsel = __umulhi(x, 1u << (16 - s));                               // x >> (16+s): low 5 bits = B' & 31
+  const uint32_t g = __umulhi(x, 1u << (13 + 2 * L));               // x >> (19-2L): G' at bit L-3
+  uint32_t c = g & (((1u << L) - 1u) << (L - 3));
+  if constexpr (L == 6) c |= __umulhi(x, 1u << (5 + L)) & 4u;        // x >> (27-L): B'5 at bit 2
+  addr = r * (Smem<L>::ROWW * 4u) + c;
 }
 
 // Pixel j (0..15) of a 48-byte unit held in w[0..11] -> [*, R, G, B]
@@ -133,6 +153,26 @@ __device__ __forceinline__ uint32_t pixel_word(const uint32_t (&w)[12]) {
   constexpr uint32_t sel = (uint32_t(b) << 4) | (uint32_t(b + 1) << 8) | (uint32_t(b + 2) << 12);
   if constexpr (a + 1 < 12) return __byte_perm(w[a], w[a + 1], sel);
   else return __byte_perm(w[a], w[a], sel);
+}
+
+// Pixel j -> [*, G, B, R] (the skewed-layout operand order)
+template <int J>
+__device__ __forceinline__ uint32_t pixel_word_gbr(const uint32_t (&w)[12]) {
+  constexpr int o = 3 * J, a = o >> 2, b = o & 3;
+  constexpr uint32_t sel = (uint32_t(b + 1) << 4) | (uint32_t(b + 2) << 8) | (uint32_t(b) << 12);
+  if constexpr (a + 1 < 12) return __byte_perm(w[a], w[a + 1], sel);
+  else return __byte_perm(w[a], w[a], sel);
+}
+
+// Pixel j in the operand order of level L's shared layout
+template <int L, int J>
+__device__ __forceinline__ uint32_t pixel_operand(const uint32_t (&w)[12]) {
+  if constexpr (Smem<L>::skew) return pixel_word_gbr<J>(w);
+  else return pixel_word<J>(w);
+}
+
+__device__ __forceinline__ uint32_t gbr_word_scalar(const uint8_t* p) {
+  return (uint32_t(p[1]) << 8) | (uint32_t(p[2]) << 16) | (uint32_t(p[0]) << 24);
 }
 
 __device__ __forceinline__ uint32_t rgb_word_scalar(const uint8_t* p) {
@@ -206,33 +246,61 @@ __device__ __forceinline__ void count_code(uint32_t* counts, uint32_t idx) {
 
 // One 16-pixel unit: all lookups first (independent LDS), then the rare
 // check-before-set atomics, so the common path is straight-line code.
+template <int L>
+__device__ __forceinline__ uint32_t operand_to_cube(uint32_t x) {
+  if constexpr (Smem<L>::skew) {
+    constexpr int s = 8 - L;
+    constexpr uint32_t M = (1u << L) - 1u;
+    return ((x >> (24 + s)) << (2 * L)) | (((x >> (8 + s)) & M) << L) | ((x >> (16 + s)) & M);
+  } else {
+    return cube_idx<L>(x);
+  }
+}
+
+// Word byte address + bit selector of operand x in the leaf bitset `bits`
+// (shared for L <= 6, global cube for L >= 7).
+template <int L>
+__device__ __forceinline__ void bit_position(uint32_t x, uint32_t& addr, uint32_t& bsel) {
+  if constexpr (Smem<L>::skew) {
+    skew_lookup<L>(x, addr, bsel);
+  } else {
+    const uint32_t idx = cube_idx<L>(x);
+    addr = (idx >> 5) << 2;
+    bsel = idx;
+  }
+}
+
+template <int J, int L>
+__device__ __forceinline__ void unpack16(const uint32_t (&w)[12], uint32_t (&px)[16]) {
+  px[J] = pixel_operand<L, J>(w);
+  if constexpr (J + 1 < 16) unpack16<J + 1, L>(w, px);
+}
+
+// One 16-pixel unit: all lookups first (independent loads), then the rare
+// check-before-set atomics, so the common path is straight-line code.
 template <int L, bool SMEM_BITS, bool COUNTS>
 __device__ __forceinline__ void build_unit(const uint32_t (&w)[12], uint32_t* bits, uint32_t* cnt) {
   uint32_t px[16];
-  px[0] = pixel_word<0>(w);   px[1] = pixel_word<1>(w);   px[2] = pixel_word<2>(w);
-  px[3] = pixel_word<3>(w);   px[4] = pixel_word<4>(w);   px[5] = pixel_word<5>(w);
-  px[6] = pixel_word<6>(w);   px[7] = pixel_word<7>(w);   px[8] = pixel_word<8>(w);
-  px[9] = pixel_word<9>(w);   px[10] = pixel_word<10>(w); px[11] = pixel_word<11>(w);
-  px[12] = pixel_word<12>(w); px[13] = pixel_word<13>(w); px[14] = pixel_word<14>(w);
-  px[15] = pixel_word<15>(w);
+  unpack16<0, L>(w, px);
+  char* base = reinterpret_cast<char*>(bits);
 #pragma unroll
   for (int h = 0; h < 16; h += 8) {
-    uint32_t sidx[8], wd[8];
+    uint32_t addr[8], bsel[8], wd[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const uint32_t idx = cube_idx<L>(px[h + j]);
-      sidx[j] = SMEM_BITS ? swizzle_idx<L>(idx, px[h + j]) : idx;
-      if constexpr (SMEM_BITS) wd[j] = bits[sidx[j] >> 5];
-      else wd[j] = *reinterpret_cast<volatile uint32_t*>(bits + (sidx[j] >> 5));
+      bit_position<L>(px[h + j], addr[j], bsel[j]);
+      if constexpr (SMEM_BITS) wd[j] = *reinterpret_cast<const uint32_t*>(base + addr[j]);
+      else wd[j] = *reinterpret_cast<volatile uint32_t*>(base + addr[j]);
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      if (!((wd[j] >> (sidx[j] & 31u)) & 1u)) atomicOr(bits + (sidx[j] >> 5), 1u << (sidx[j] & 31u));
+      if (!(__funnelshift_r(wd[j], wd[j], bsel[j]) & 1u))
+        atomicOr(reinterpret_cast<uint32_t*>(base + addr[j]), 1u << (bsel[j] & 31u));
     }
   }
   if constexpr (COUNTS) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) count_code<L>(cnt, cube_idx<L>(px[j]));
+    for (int j = 0; j < 16; ++j) count_code<L>(cnt, operand_to_cube<L>(px[j]));
   }
 }
 
@@ -247,7 +315,7 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
   const int64_t u_end = min(total_units, u_begin + units_per_cta);
   if (u_begin >= u_end) return;
   if constexpr (SMEM_BITS) {
-    for (int i = threadIdx.x; i < CW; i += BUILD_BLOCK) s_bits[i] = 0u;
+    for (int i = threadIdx.x; i < Smem<L>::words; i += BUILD_BLOCK) s_bits[i] = 0u;
     __syncthreads();
   }
   const int64_t units_per_tree = units_per_frame * group_size;
@@ -271,9 +339,9 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
     if constexpr (SMEM_BITS) {
       __syncthreads();
       uint32_t* dst = ws + tree * CW;
-      for (int i = threadIdx.x; i < CW; i += BUILD_BLOCK) {
-        uint32_t x = s_bits[i];
-        if (x) { atomicOr(dst + Swz<L>::word(i), x); s_bits[i] = 0u; }
+      for (int i = threadIdx.x; i < Smem<L>::words; i += BUILD_BLOCK) {
+        const uint32_t x = s_bits[i];
+        if (x) { atomicOr(dst + Smem<L>::canon(i), x); s_bits[i] = 0u; }   // pad words stay 0
       }
       __syncthreads();
     }
@@ -641,24 +709,16 @@ template <int L, bool SMEM_BITS, bool PACKED>
 __device__ __forceinline__ void classify_unit(const uint32_t (&w)[12], const uint32_t* bits, uint8_t* mask,
                                               int64_t u) {
   uint32_t px[16];
-  px[0] = pixel_word<0>(w);   px[1] = pixel_word<1>(w);   px[2] = pixel_word<2>(w);
-  px[3] = pixel_word<3>(w);   px[4] = pixel_word<4>(w);   px[5] = pixel_word<5>(w);
-  px[6] = pixel_word<6>(w);   px[7] = pixel_word<7>(w);   px[8] = pixel_word<8>(w);
-  px[9] = pixel_word<9>(w);   px[10] = pixel_word<10>(w); px[11] = pixel_word<11>(w);
-  px[12] = pixel_word<12>(w); px[13] = pixel_word<13>(w); px[14] = pixel_word<14>(w);
-  px[15] = pixel_word<15>(w);
+  unpack16<0, L>(w, px);
+  const char* base = reinterpret_cast<const char*>(bits);
   uint32_t v[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
-    uint32_t idx = cube_idx<L>(px[j]);
-    uint32_t wd;
-    if constexpr (SMEM_BITS) {
-      idx = swizzle_idx<L>(idx, px[j]);
-      wd = bits[idx >> 5];
-    } else {
-      wd = __ldg(bits + (idx >> 5));
-    }
-    v[j] = __funnelshift_r(wd, wd, idx);      // bit 0 = background
+    uint32_t addr, bsel, wd;
+    bit_position<L>(px[j], addr, bsel);
+    if constexpr (SMEM_BITS) wd = *reinterpret_cast<const uint32_t*>(base + addr);
+    else wd = __ldg(reinterpret_cast<const uint32_t*>(base + addr));
+    v[j] = __funnelshift_r(wd, wd, bsel);      // bit 0 = background
   }
   if constexpr (!PACKED) {
     uint4 o;
@@ -685,7 +745,7 @@ k_classify_flat(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_p
   constexpr int64_t CW = cube_words(L);
   const uint32_t* bits = cube;
   if constexpr (SMEM_BITS) {
-    for (int i = threadIdx.x; i < CW; i += CLS_BLOCK) s_bits[Swz<L>::word(i)] = __ldg(cube + i);
+    for (int i = threadIdx.x; i < CW; i += CLS_BLOCK) s_bits[Smem<L>::phys(i)] = __ldg(cube + i);
     __syncthreads();
     bits = s_bits;
   }
@@ -703,10 +763,12 @@ k_classify_flat(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_p
   if constexpr (!PACKED) {
     if (blockIdx.x == 0) {
       for (int64_t i = n_units * 16 + threadIdx.x; i < n_pixels; i += CLS_BLOCK) {
-        const uint32_t x = rgb_word_scalar(frames + 3 * i);
-        const uint32_t idx = SMEM_BITS ? swizzle_idx<L>(cube_idx<L>(x), x) : cube_idx<L>(x);
-        const uint32_t wd = SMEM_BITS ? bits[idx >> 5] : __ldg(bits + (idx >> 5));
-        mask[i] = uint8_t(((wd >> (idx & 31u)) & 1u) ^ 1u);
+        const uint32_t x = Smem<L>::skew ? gbr_word_scalar(frames + 3 * i) : rgb_word_scalar(frames + 3 * i);
+        uint32_t addr, bsel;
+        bit_position<L>(x, addr, bsel);
+        const uint32_t* wp = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(bits) + addr);
+        const uint32_t wd = SMEM_BITS ? *wp : __ldg(wp);
+        mask[i] = uint8_t(((wd >> (bsel & 31u)) & 1u) ^ 1u);
       }
     }
   }
@@ -870,7 +932,7 @@ template <int L>
 static int launch_build_flat(const uint8_t* frames, int64_t units_per_frame, int64_t total_units, int group_size,
                              uint32_t* ws, uint32_t* counts, cudaStream_t st) {
   constexpr bool SMEM = L <= 6;
-  const size_t smem = SMEM ? size_t(cube_words(L)) * 4 : 0;
+  const size_t smem = SMEM ? size_t(Smem<L>::words) * 4 : 0;
   int blocks_per_sm;
   if (counts) {
     auto k = k_build_flat<L, SMEM, true>;
@@ -1051,7 +1113,7 @@ template <int L>
 static int launch_classify_flat(const uint8_t* frames, int64_t n_pixels, const uint32_t* cube, uint8_t* mask,
                                 bool packed, cudaStream_t st) {
   constexpr bool SMEM = L <= 6;
-  const size_t smem = SMEM ? size_t(cube_words(L)) * 4 : 0;
+  const size_t smem = SMEM ? size_t(Smem<L>::words) * 4 : 0;
   const int64_t n_units = n_pixels / 16;
   int bps;
   if (packed) bps = occupancy(k_classify_flat<L, SMEM, true>, CLS_BLOCK, smem);
