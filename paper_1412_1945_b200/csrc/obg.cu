@@ -276,28 +276,51 @@ __device__ __forceinline__ void unpack16(const uint32_t (&w)[12], uint32_t (&px)
   if constexpr (J + 1 < 16) unpack16<J + 1, L>(w, px);
 }
 
-// One 16-pixel unit: all lookups first (independent loads), then the rare
-// check-before-set atomics, so the common path is straight-line code.
+// Presence bits of 16 pixels packed one per byte (bit 0 of byte k of word q
+// = pixel 4q+k), the same PRMT packing the classify kernel uses.
+__device__ __forceinline__ uint4 pack_presence(const uint32_t (&v)[16]) {
+  uint4 o;
+  o.x = __byte_perm(__byte_perm(v[0], v[1], 0x0040), __byte_perm(v[2], v[3], 0x0040), 0x5410);
+  o.y = __byte_perm(__byte_perm(v[4], v[5], 0x0040), __byte_perm(v[6], v[7], 0x0040), 0x5410);
+  o.z = __byte_perm(__byte_perm(v[8], v[9], 0x0040), __byte_perm(v[10], v[11], 0x0040), 0x5410);
+  o.w = __byte_perm(__byte_perm(v[12], v[13], 0x0040), __byte_perm(v[14], v[15], 0x0040), 0x5410);
+  return o;
+}
+
+// Rare path: set the bits of the pixels whose presence bit was clear.  The
+// operands are re-derived from the raw words so that only w[] and the packed
+// presence stay live across the common path.
+template <int L, int J>
+__device__ __forceinline__ void build_unit_slow(const uint32_t (&w)[12], const uint4& o, char* base) {
+  const uint32_t q = J < 4 ? o.x : J < 8 ? o.y : J < 12 ? o.z : o.w;
+  if (!((q >> (8 * (J & 3))) & 1u)) {
+    uint32_t addr, bsel;
+    bit_position<L>(pixel_operand<L, J>(w), addr, bsel);
+    atomicOr(reinterpret_cast<uint32_t*>(base + addr), 1u << (bsel & 31u));
+  }
+  if constexpr (J + 1 < 16) build_unit_slow<L, J + 1>(w, o, base);
+}
+
+// One 16-pixel unit: 16 independent lookups, presence packed into one
+// all-present test; only a unit holding a colour this CTA has not recorded
+// yet takes the (rare) check-before-set atomic path.
 template <int L, bool SMEM_BITS, bool COUNTS>
 __device__ __forceinline__ void build_unit(const uint32_t (&w)[12], uint32_t* bits, uint32_t* cnt) {
   uint32_t px[16];
   unpack16<0, L>(w, px);
   char* base = reinterpret_cast<char*>(bits);
+  uint32_t v[16];
 #pragma unroll
-  for (int h = 0; h < 16; h += 8) {
-    uint32_t addr[8], bsel[8], wd[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      bit_position<L>(px[h + j], addr[j], bsel[j]);
-      if constexpr (SMEM_BITS) wd[j] = *reinterpret_cast<const uint32_t*>(base + addr[j]);
-      else wd[j] = *reinterpret_cast<volatile uint32_t*>(base + addr[j]);
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (!(__funnelshift_r(wd[j], wd[j], bsel[j]) & 1u))
-        atomicOr(reinterpret_cast<uint32_t*>(base + addr[j]), 1u << (bsel[j] & 31u));
-    }
+  for (int j = 0; j < 16; ++j) {
+    uint32_t addr, bsel, wd;
+    bit_position<L>(px[j], addr, bsel);
+    if constexpr (SMEM_BITS) wd = *reinterpret_cast<const uint32_t*>(base + addr);
+    else wd = *reinterpret_cast<volatile uint32_t*>(base + addr);
+    v[j] = __funnelshift_r(wd, wd, bsel);
   }
+  const uint4 o = pack_presence(v);
+  if ((o.x & o.y & o.z & o.w & 0x01010101u) != 0x01010101u)
+    build_unit_slow<L, 0>(w, o, base);
   if constexpr (COUNTS) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) count_code<L>(cnt, operand_to_cube<L>(px[j]));
@@ -305,7 +328,7 @@ __device__ __forceinline__ void build_unit(const uint32_t (&w)[12], uint32_t* bi
 }
 
 template <int L, bool SMEM_BITS, bool COUNTS>
-__global__ void __launch_bounds__(BUILD_BLOCK)
+__global__ void __launch_bounds__(BUILD_BLOCK, SMEM_BITS ? 2 : 1)
 k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t total_units,
              int group_size, int64_t units_per_cta, uint32_t* __restrict__ ws,
              uint32_t* __restrict__ counts) {
