@@ -287,18 +287,48 @@ __device__ __forceinline__ uint4 pack_presence(const uint32_t (&v)[16]) {
   return o;
 }
 
-// Rare path: set the bits of the pixels whose presence bit was clear.  The
-// operands are re-derived from the raw words so that only w[] and the packed
-// presence stay live across the common path.
+// Rare path of one pixel position: set its bit (lanes whose pixel J missed).
 template <int L, int J>
+__device__ __forceinline__ void set_pixel_bit(const uint32_t (&w)[12], char* base) {
+  uint32_t addr, bsel;
+  bit_position<L>(pixel_operand<L, J>(w), addr, bsel);
+  atomicOr(reinterpret_cast<uint32_t*>(base + addr), 1u << (bsel & 31u));
+}
+
+// Missing pixels of a unit: the warp walks the union of its lanes' miss
+// positions (warp-uniform, usually 1-3 of 16) and dispatches with a switch,
+// so a miss costs ~a dozen instructions instead of re-deriving all 16 pixels
+// under divergence (ncu r5: that path cost 5 instr/px).
+template <int L>
 __device__ __forceinline__ void build_unit_slow(const uint32_t (&w)[12], const uint4& o, char* base) {
-  const uint32_t q = J < 4 ? o.x : J < 8 ? o.y : J < 12 ? o.z : o.w;
-  if (!((q >> (8 * (J & 3))) & 1u)) {
-    uint32_t addr, bsel;
-    bit_position<L>(pixel_operand<L, J>(w), addr, bsel);
-    atomicOr(reinterpret_cast<uint32_t*>(base + addr), 1u << (bsel & 31u));
+  const uint32_t q0 = (o.x & 0x01010101u) * 0x10204080u >> 28, q1 = (o.y & 0x01010101u) * 0x10204080u >> 28;
+  const uint32_t q2 = (o.z & 0x01010101u) * 0x10204080u >> 28, q3 = (o.w & 0x01010101u) * 0x10204080u >> 28;
+  const uint32_t miss = ~(q0 | (q1 << 4) | (q2 << 8) | (q3 << 12)) & 0xFFFFu;
+  uint32_t wmiss = __reduce_or_sync(__activemask(), miss);
+  while (wmiss) {
+    const int j = __ffs(wmiss) - 1;
+    wmiss &= wmiss - 1;
+    if ((miss >> j) & 1u) {
+      switch (j) {
+        case 0: set_pixel_bit<L, 0>(w, base); break;
+        case 1: set_pixel_bit<L, 1>(w, base); break;
+        case 2: set_pixel_bit<L, 2>(w, base); break;
+        case 3: set_pixel_bit<L, 3>(w, base); break;
+        case 4: set_pixel_bit<L, 4>(w, base); break;
+        case 5: set_pixel_bit<L, 5>(w, base); break;
+        case 6: set_pixel_bit<L, 6>(w, base); break;
+        case 7: set_pixel_bit<L, 7>(w, base); break;
+        case 8: set_pixel_bit<L, 8>(w, base); break;
+        case 9: set_pixel_bit<L, 9>(w, base); break;
+        case 10: set_pixel_bit<L, 10>(w, base); break;
+        case 11: set_pixel_bit<L, 11>(w, base); break;
+        case 12: set_pixel_bit<L, 12>(w, base); break;
+        case 13: set_pixel_bit<L, 13>(w, base); break;
+        case 14: set_pixel_bit<L, 14>(w, base); break;
+        default: set_pixel_bit<L, 15>(w, base); break;
+      }
+    }
   }
-  if constexpr (J + 1 < 16) build_unit_slow<L, J + 1>(w, o, base);
 }
 
 // One 16-pixel unit: 16 independent lookups, presence packed into one
@@ -319,8 +349,8 @@ __device__ __forceinline__ void build_unit(const uint32_t (&w)[12], uint32_t* bi
     v[j] = __funnelshift_r(wd, wd, bsel);
   }
   const uint4 o = pack_presence(v);
-  if ((o.x & o.y & o.z & o.w & 0x01010101u) != 0x01010101u)
-    build_unit_slow<L, 0>(w, o, base);
+  if (__any_sync(__activemask(), (o.x & o.y & o.z & o.w & 0x01010101u) != 0x01010101u))
+    build_unit_slow<L>(w, o, base);
   if constexpr (COUNTS) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) count_code<L>(cnt, operand_to_cube<L>(px[j]));
