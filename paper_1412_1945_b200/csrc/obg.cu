@@ -276,89 +276,45 @@ __device__ __forceinline__ void unpack16(const uint32_t (&w)[12], uint32_t (&px)
   if constexpr (J + 1 < 16) unpack16<J + 1, L>(w, px);
 }
 
-// Presence bits of 16 pixels packed one per byte (bit 0 of byte k of word q
-// = pixel 4q+k), the same PRMT packing the classify kernel uses.
-__device__ __forceinline__ uint4 pack_presence(const uint32_t (&v)[16]) {
-  uint4 o;
-  o.x = __byte_perm(__byte_perm(v[0], v[1], 0x0040), __byte_perm(v[2], v[3], 0x0040), 0x5410);
-  o.y = __byte_perm(__byte_perm(v[4], v[5], 0x0040), __byte_perm(v[6], v[7], 0x0040), 0x5410);
-  o.z = __byte_perm(__byte_perm(v[8], v[9], 0x0040), __byte_perm(v[10], v[11], 0x0040), 0x5410);
-  o.w = __byte_perm(__byte_perm(v[12], v[13], 0x0040), __byte_perm(v[14], v[15], 0x0040), 0x5410);
-  return o;
-}
-
-// Rare path of one pixel position: set its bit (lanes whose pixel J missed).
-template <int L, int J>
-__device__ __forceinline__ void set_pixel_bit(const uint32_t (&w)[12], char* base) {
-  uint32_t addr, bsel;
-  bit_position<L>(pixel_operand<L, J>(w), addr, bsel);
-  atomicOr(reinterpret_cast<uint32_t*>(base + addr), 1u << (bsel & 31u));
-}
-
-// Missing pixels of a unit: the warp walks the union of its lanes' miss
-// positions (warp-uniform, usually 1-3 of 16) and dispatches with a switch,
-// so a miss costs ~a dozen instructions instead of re-deriving all 16 pixels
-// under divergence (ncu r5: that path cost 5 instr/px).
-template <int L>
-__device__ __forceinline__ void build_unit_slow(const uint32_t (&w)[12], const uint4& o, char* base) {
-  const uint32_t q0 = (o.x & 0x01010101u) * 0x10204080u >> 28, q1 = (o.y & 0x01010101u) * 0x10204080u >> 28;
-  const uint32_t q2 = (o.z & 0x01010101u) * 0x10204080u >> 28, q3 = (o.w & 0x01010101u) * 0x10204080u >> 28;
-  const uint32_t miss = ~(q0 | (q1 << 4) | (q2 << 8) | (q3 << 12)) & 0xFFFFu;
-  uint32_t wmiss = __reduce_or_sync(__activemask(), miss);
-  while (wmiss) {
-    const int j = __ffs(wmiss) - 1;
-    wmiss &= wmiss - 1;
-    if ((miss >> j) & 1u) {
-      switch (j) {
-        case 0: set_pixel_bit<L, 0>(w, base); break;
-        case 1: set_pixel_bit<L, 1>(w, base); break;
-        case 2: set_pixel_bit<L, 2>(w, base); break;
-        case 3: set_pixel_bit<L, 3>(w, base); break;
-        case 4: set_pixel_bit<L, 4>(w, base); break;
-        case 5: set_pixel_bit<L, 5>(w, base); break;
-        case 6: set_pixel_bit<L, 6>(w, base); break;
-        case 7: set_pixel_bit<L, 7>(w, base); break;
-        case 8: set_pixel_bit<L, 8>(w, base); break;
-        case 9: set_pixel_bit<L, 9>(w, base); break;
-        case 10: set_pixel_bit<L, 10>(w, base); break;
-        case 11: set_pixel_bit<L, 11>(w, base); break;
-        case 12: set_pixel_bit<L, 12>(w, base); break;
-        case 13: set_pixel_bit<L, 13>(w, base); break;
-        case 14: set_pixel_bit<L, 14>(w, base); break;
-        default: set_pixel_bit<L, 15>(w, base); break;
-      }
+// One 16-pixel unit, called by all 32 lanes of a warp (`valid` false for
+// lanes past the segment).  Lookups go in groups of four; a group takes the
+// atomic path only if some lane of the warp misses one of its pixels -- a
+// warp-uniform branch, so the common path has no divergence (ncu r4-r6:
+// per-pixel divergent branches cost ~5 instructions/pixel).  About 0.45 % of
+// pixels miss at C3 (first occurrences of a colour within a CTA's range).
+template <int L, bool SMEM_BITS, bool COUNTS>
+__device__ __forceinline__ void build_unit(const uint32_t (&w)[12], uint32_t* bits, uint32_t* cnt, bool valid) {
+  uint32_t px[16];
+  unpack16<0, L>(w, px);
+  char* base = reinterpret_cast<char*>(bits);
+#pragma unroll
+  for (int g = 0; g < 16; g += 4) {
+    uint32_t addr[4], bsel[4], v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint32_t wd;
+      bit_position<L>(px[g + j], addr[j], bsel[j]);
+      if constexpr (SMEM_BITS) wd = *reinterpret_cast<const uint32_t*>(base + addr[j]);
+      else wd = *reinterpret_cast<volatile uint32_t*>(base + addr[j]);
+      v[j] = __funnelshift_r(wd, wd, bsel[j]);
+    }
+    const bool miss = valid && !(v[0] & v[1] & v[2] & v[3] & 1u);
+    if (__any_sync(0xFFFFFFFFu, miss)) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (valid && !(v[j] & 1u)) atomicOr(reinterpret_cast<uint32_t*>(base + addr[j]), 1u << (bsel[j] & 31u));
+    }
+  }
+  if constexpr (COUNTS) {
+    if (valid) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) count_code<L>(cnt, operand_to_cube<L>(px[j]));
     }
   }
 }
 
-// One 16-pixel unit: 16 independent lookups, presence packed into one
-// all-present test; only a unit holding a colour this CTA has not recorded
-// yet takes the (rare) check-before-set atomic path.
 template <int L, bool SMEM_BITS, bool COUNTS>
-__device__ __forceinline__ void build_unit(const uint32_t (&w)[12], uint32_t* bits, uint32_t* cnt) {
-  uint32_t px[16];
-  unpack16<0, L>(w, px);
-  char* base = reinterpret_cast<char*>(bits);
-  uint32_t v[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    uint32_t addr, bsel, wd;
-    bit_position<L>(px[j], addr, bsel);
-    if constexpr (SMEM_BITS) wd = *reinterpret_cast<const uint32_t*>(base + addr);
-    else wd = *reinterpret_cast<volatile uint32_t*>(base + addr);
-    v[j] = __funnelshift_r(wd, wd, bsel);
-  }
-  const uint4 o = pack_presence(v);
-  if (__any_sync(__activemask(), (o.x & o.y & o.z & o.w & 0x01010101u) != 0x01010101u))
-    build_unit_slow<L>(w, o, base);
-  if constexpr (COUNTS) {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) count_code<L>(cnt, operand_to_cube<L>(px[j]));
-  }
-}
-
-template <int L, bool SMEM_BITS, bool COUNTS>
-__global__ void __launch_bounds__(BUILD_BLOCK, SMEM_BITS ? 2 : 1)
+__global__ void __launch_bounds__(BUILD_BLOCK, 2)
 k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t total_units,
              int group_size, int64_t units_per_cta, uint32_t* __restrict__ ws,
              uint32_t* __restrict__ counts) {
@@ -380,14 +336,18 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
     if constexpr (SMEM_BITS) bits = s_bits;
     else bits = ws + tree * CW;
     uint32_t* cnt = COUNTS ? counts + tree * (int64_t(1) << (3 * L)) : nullptr;
-    // two units per thread and iteration: six 16-byte loads in flight
-    for (int64_t v = u + threadIdx.x; v < seg_end; v += 2 * BUILD_BLOCK) {
-      const bool second = v + BUILD_BLOCK < seg_end;
+    // Two units per thread and iteration (six 16-byte loads in flight).  The
+    // trip count is warp-uniform (lanes past the segment carry valid=false) so
+    // that build_unit can branch on warp votes.
+    const int lane = threadIdx.x & 31;
+    for (int64_t wv = u + threadIdx.x - lane; wv < seg_end; wv += 2 * BUILD_BLOCK) {
+      const int64_t v = wv + lane;
+      const bool first = v < seg_end, second = v + BUILD_BLOCK < seg_end;
       uint32_t wa[12], wb[12];
-      load_unit(frames, v, wa);
+      if (first) load_unit(frames, v, wa);
       if (second) load_unit(frames, v + BUILD_BLOCK, wb);
-      build_unit<L, SMEM_BITS, COUNTS>(wa, bits, cnt);
-      if (second) build_unit<L, SMEM_BITS, COUNTS>(wb, bits, cnt);
+      build_unit<L, SMEM_BITS, COUNTS>(wa, bits, cnt, first);
+      if (__any_sync(0xFFFFFFFFu, second)) build_unit<L, SMEM_BITS, COUNTS>(wb, bits, cnt, second);
     }
     if constexpr (SMEM_BITS) {
       __syncthreads();
