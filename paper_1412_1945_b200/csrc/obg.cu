@@ -94,6 +94,15 @@ __host__ __device__ static inline uint32_t code_to_cube(uint32_t code, int L) {
   return (compact3(code >> 2) << (2 * L)) | (compact3(code >> 1) << L) | compact3(code);
 }
 
+// nz4(w): bit q set iff byte q of w is non-zero
+__device__ __forceinline__ uint32_t nz4(uint32_t w) {
+  uint32_t t = w | (w >> 4);
+  t |= t >> 2;
+  t |= t >> 1;
+  t &= 0x01010101u;
+  return (t * 0x10204080u) >> 28;
+}
+
 // x holds bytes [*, R, G, B] (byte 0 ignored).  Returns R'<<2L | G'<<L | B'.
 template <int L>
 __device__ __forceinline__ uint32_t cube_idx(uint32_t x) {
@@ -282,11 +291,17 @@ __device__ __forceinline__ void unpack16(const uint32_t (&w)[12], uint32_t (&px)
 // warp-uniform branch, so the common path has no divergence (ncu r4-r6:
 // per-pixel divergent branches cost ~5 instructions/pixel).  About 0.45 % of
 // pixels miss at C3 (first occurrences of a colour within a CTA's range).
+__device__ __forceinline__ uint32_t* dyn_smem() {
+  extern __shared__ uint32_t s_dyn[];
+  return s_dyn;
+}
+
 template <int L, bool SMEM_BITS, bool COUNTS>
 __device__ __forceinline__ void build_unit(const uint32_t (&w)[12], uint32_t* bits, uint32_t* cnt, bool valid) {
   uint32_t px[16];
   unpack16<0, L>(w, px);
-  char* base = reinterpret_cast<char*>(bits);
+  // the shared window base is known statically; lets ptxas fold it into LDS
+  char* base = SMEM_BITS ? reinterpret_cast<char*>(dyn_smem()) : reinterpret_cast<char*>(bits);
 #pragma unroll
   for (int g = 0; g < 16; g += 4) {
     uint32_t addr[4], bsel[4], v[4];
@@ -313,11 +328,65 @@ __device__ __forceinline__ void build_unit(const uint32_t (&w)[12], uint32_t* bi
   }
 }
 
+// Path-order leaf word m (codes 32m..32m+31) of the shared cube bitset:
+// 8 nibble gathers (see morton_word_from_cube), through the shared layout.
+template <int L>
+__device__ __forceinline__ uint32_t morton_word_from_smem(const uint32_t* s, uint32_t m) {
+  if constexpr (L == 1) {
+    return s[0] & 0xFFu;        // cube index == path code
+  } else {
+    const uint32_t base = code_to_cube(m << 5, L);
+    uint32_t out = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t g0 = c & 1, r0 = (c >> 1) & 1, g1 = (c >> 2) & 1;
+      const uint32_t idx = base + ((g0 | (g1 << 1)) << L) + (r0 << (2 * L));
+      const uint32_t nib = (s[Smem<L>::phys(idx >> 5)] >> (idx & 31u)) & 0xFu;
+      out |= ((nib & 3u) | ((nib & 12u) << 6)) << (g0 * 2 + r0 * 4 + g1 * 16);
+    }
+    return out;
+  }
+}
+
+// End of a CTA's segment of one tree: convert the shared cube bitset to the
+// tree's path-order pyramid in a shared scratch pyramid (leaf level, then each
+// interior level as the byte-wise OR of its children), OR its non-zero words
+// into `out` (zeroed by the host; several CTAs contribute to one tree) and
+// re-zero the cube for the next segment.  Replaces a workspace round trip +
+// separate pyramid kernel (ncu r4: 10.7 us + a 2 MB memset per build).
+template <int L>
+__device__ __forceinline__ void flush_pyramid(uint32_t* s, uint32_t* out) {
+  constexpr int64_t LW = level_words(L);
+  uint32_t* P = s + Smem<L>::words;                 // scratch pyramid, pyr_words(L) words
+  const int t = threadIdx.x;
+  __syncthreads();
+  for (int64_t m = t; m < LW; m += BUILD_BLOCK) P[level_offset(L) + m] = morton_word_from_smem<L>(s, uint32_t(m));
+  __syncthreads();
+  for (int i = t; i < Smem<L>::words; i += BUILD_BLOCK) s[i] = 0u;
+  for (int l = L - 1; l >= 1; --l) {
+    const int64_t off = level_offset(l), coff = level_offset(l + 1), cw = level_words(l + 1);
+    for (int64_t k = t; k < level_words(l); k += BUILD_BLOCK) {
+      uint32_t x = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (8 * k + q < cw) x |= nz4(P[coff + 8 * k + q]) << (4 * q);
+      P[off + k] = x;
+    }
+    __syncthreads();
+  }
+  for (int64_t i = t; i < pyr_words(L); i += BUILD_BLOCK) {
+    uint32_t x = P[i];
+    if (L == 1) x &= 0xFFu;
+    if (x) atomicOr(out + i, x);
+  }
+  __syncthreads();
+}
+
 template <int L, bool SMEM_BITS, bool COUNTS>
 __global__ void __launch_bounds__(BUILD_BLOCK, 2)
 k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t total_units,
              int group_size, int64_t units_per_cta, uint32_t* __restrict__ ws,
-             uint32_t* __restrict__ counts) {
+             uint32_t* __restrict__ out_pyr, uint32_t* __restrict__ counts) {
   extern __shared__ uint32_t s_bits[];
   constexpr int64_t CW = cube_words(L);
   const int64_t u_begin = int64_t(blockIdx.x) * units_per_cta;
@@ -349,15 +418,7 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
       build_unit<L, SMEM_BITS, COUNTS>(wa, bits, cnt, first);
       if (__any_sync(0xFFFFFFFFu, second)) build_unit<L, SMEM_BITS, COUNTS>(wb, bits, cnt, second);
     }
-    if constexpr (SMEM_BITS) {
-      __syncthreads();
-      uint32_t* dst = ws + tree * CW;
-      for (int i = threadIdx.x; i < Smem<L>::words; i += BUILD_BLOCK) {
-        const uint32_t x = s_bits[i];
-        if (x) { atomicOr(dst + Smem<L>::canon(i), x); s_bits[i] = 0u; }   // pad words stay 0
-      }
-      __syncthreads();
-    }
+    if constexpr (SMEM_BITS) flush_pyramid<L>(s_bits, out_pyr + tree * pyr_words(L));
     u = seg_end;
   }
 }
@@ -414,15 +475,6 @@ __device__ __forceinline__ uint32_t morton_word_from_cube(const uint32_t* __rest
     out |= sp << (g0 * 2 + r0 * 4 + g1 * 16);
   }
   return out;
-}
-
-// nz4(w): bit q set iff byte q of w is non-zero
-__device__ __forceinline__ uint32_t nz4(uint32_t w) {
-  uint32_t t = w | (w >> 4);
-  t |= t >> 2;
-  t |= t >> 1;
-  t &= 0x01010101u;
-  return (t * 0x10204080u) >> 28;
 }
 
 template <bool FROM_CUBE>
@@ -943,16 +995,22 @@ int obg_pack_codes(const uint8_t* pixels, int64_t n_pixels, int levels, uint32_t
 
 template <int L>
 static int launch_build_flat(const uint8_t* frames, int64_t units_per_frame, int64_t total_units, int group_size,
-                             uint32_t* ws, uint32_t* counts, cudaStream_t st) {
+                             uint32_t* ws, uint32_t* out_pyr, uint32_t* counts, cudaStream_t st) {
   constexpr bool SMEM = L <= 6;
-  const size_t smem = SMEM ? size_t(Smem<L>::words) * 4 : 0;
-  int blocks_per_sm;
-  if (counts) {
-    auto k = k_build_flat<L, SMEM, true>;
-    blocks_per_sm = occupancy(k, BUILD_BLOCK, smem);
-  } else {
-    auto k = k_build_flat<L, SMEM, false>;
-    blocks_per_sm = occupancy(k, BUILD_BLOCK, smem);
+  const size_t smem = SMEM ? size_t(Smem<L>::words + pyr_words(L)) * 4 : 0;   // cube + scratch pyramid
+  // one-time per instantiation: opt in to > 48 KB dynamic smem, cache occupancy
+  static int occ[2] = {0, 0};
+  int& blocks_per_sm = occ[counts ? 1 : 0];
+  if (blocks_per_sm == 0) {
+    if (counts) {
+      auto k = k_build_flat<L, SMEM, true>;
+      CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      blocks_per_sm = occupancy(k, BUILD_BLOCK, smem);
+    } else {
+      auto k = k_build_flat<L, SMEM, false>;
+      CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      blocks_per_sm = occupancy(k, BUILD_BLOCK, smem);
+    }
   }
   const int64_t max_ctas = int64_t(sm_count()) * blocks_per_sm;
   // at least 4 units per thread per CTA so that tiny inputs use few CTAs
@@ -962,10 +1020,10 @@ static int launch_build_flat(const uint8_t* frames, int64_t units_per_frame, int
   const int grid = int((total_units + per_cta - 1) / per_cta);
   if (counts)
     k_build_flat<L, SMEM, true><<<grid, BUILD_BLOCK, smem, st>>>(frames, units_per_frame, total_units, group_size,
-                                                                 per_cta, ws, counts);
+                                                                 per_cta, ws, out_pyr, counts);
   else
     k_build_flat<L, SMEM, false><<<grid, BUILD_BLOCK, smem, st>>>(frames, units_per_frame, total_units, group_size,
-                                                                  per_cta, ws, nullptr);
+                                                                  per_cta, ws, out_pyr, nullptr);
   LAUNCH_CHECK("k_build_flat");
   return OBG_OK;
 }
@@ -1004,25 +1062,27 @@ int obg_build_presence(const uint8_t* frames, int n_frames, int height, int widt
   uint32_t* ws = static_cast<uint32_t*>(workspace);
   const int64_t CW = cube_words(levels);
   const int64_t PW = pyr_words(levels);
-  CUDA_TRY(cudaMemsetAsync(ws, 0, size_t(n_trees * CW * 4), st));
-  CUDA_TRY(cudaMemsetAsync(out_pyramids, 0, size_t(n_trees * PW * 4), st));
-  if (out_counts) CUDA_TRY(cudaMemsetAsync(out_counts, 0, size_t(n_trees) * (size_t(1) << (3 * levels)) * 4, st));
-
   const int64_t P = int64_t(height) * width;
   const int64_t used_pixels = int64_t(n_groups) * group_size * P;
   const bool flat = n_regions == 1 && (P % 16) == 0 && (reinterpret_cast<uintptr_t>(frames) % 16) == 0;
+  // flat path with a shared-memory bitset (L <= 6) writes the pyramids
+  // directly; everything else goes through the cube workspace + k_pyramid
+  const bool direct = flat && levels <= 6;
+  if (!direct) CUDA_TRY(cudaMemsetAsync(ws, 0, size_t(n_trees * CW * 4), st));
+  CUDA_TRY(cudaMemsetAsync(out_pyramids, 0, size_t(n_trees * PW * 4), st));
+  if (out_counts) CUDA_TRY(cudaMemsetAsync(out_counts, 0, size_t(n_trees) * (size_t(1) << (3 * levels)) * 4, st));
   int rc = OBG_OK;
   if (flat) {
     const int64_t upf = P / 16, total_units = used_pixels / 16;
     switch (levels) {
-      case 1: rc = launch_build_flat<1>(frames, upf, total_units, group_size, ws, out_counts, st); break;
-      case 2: rc = launch_build_flat<2>(frames, upf, total_units, group_size, ws, out_counts, st); break;
-      case 3: rc = launch_build_flat<3>(frames, upf, total_units, group_size, ws, out_counts, st); break;
-      case 4: rc = launch_build_flat<4>(frames, upf, total_units, group_size, ws, out_counts, st); break;
-      case 5: rc = launch_build_flat<5>(frames, upf, total_units, group_size, ws, out_counts, st); break;
-      case 6: rc = launch_build_flat<6>(frames, upf, total_units, group_size, ws, out_counts, st); break;
-      case 7: rc = launch_build_flat<7>(frames, upf, total_units, group_size, ws, out_counts, st); break;
-      default: rc = launch_build_flat<8>(frames, upf, total_units, group_size, ws, out_counts, st); break;
+      case 1: rc = launch_build_flat<1>(frames, upf, total_units, group_size, ws, out_pyramids, out_counts, st); break;
+      case 2: rc = launch_build_flat<2>(frames, upf, total_units, group_size, ws, out_pyramids, out_counts, st); break;
+      case 3: rc = launch_build_flat<3>(frames, upf, total_units, group_size, ws, out_pyramids, out_counts, st); break;
+      case 4: rc = launch_build_flat<4>(frames, upf, total_units, group_size, ws, out_pyramids, out_counts, st); break;
+      case 5: rc = launch_build_flat<5>(frames, upf, total_units, group_size, ws, out_pyramids, out_counts, st); break;
+      case 6: rc = launch_build_flat<6>(frames, upf, total_units, group_size, ws, out_pyramids, out_counts, st); break;
+      case 7: rc = launch_build_flat<7>(frames, upf, total_units, group_size, ws, out_pyramids, out_counts, st); break;
+      default: rc = launch_build_flat<8>(frames, upf, total_units, group_size, ws, out_pyramids, out_counts, st); break;
     }
   } else {
     const int grid = grid_for(used_pixels, 256, sm_count() * 8);
@@ -1035,6 +1095,7 @@ int obg_build_presence(const uint8_t* frames, int n_frames, int height, int widt
     LAUNCH_CHECK("k_build_generic");
   }
   if (rc != OBG_OK) return rc;
+  if (direct) return OBG_OK;
   return launch_pyramid(ws, CW, true, n_trees, levels, out_pyramids, st);
 }
 
@@ -1128,9 +1189,10 @@ static int launch_classify_flat(const uint8_t* frames, int64_t n_pixels, const u
   constexpr bool SMEM = L <= 6;
   const size_t smem = SMEM ? size_t(Smem<L>::words) * 4 : 0;
   const int64_t n_units = n_pixels / 16;
-  int bps;
-  if (packed) bps = occupancy(k_classify_flat<L, SMEM, true>, CLS_BLOCK, smem);
-  else bps = occupancy(k_classify_flat<L, SMEM, false>, CLS_BLOCK, smem);
+  static int occ[2] = {0, 0};
+  int& bps = occ[packed ? 1 : 0];
+  if (bps == 0) bps = packed ? occupancy(k_classify_flat<L, SMEM, true>, CLS_BLOCK, smem)
+                             : occupancy(k_classify_flat<L, SMEM, false>, CLS_BLOCK, smem);
   int64_t grid = int64_t(sm_count()) * bps;
   const int64_t need = (n_units + CLS_BLOCK - 1) / CLS_BLOCK;
   if (grid > need) grid = need;
