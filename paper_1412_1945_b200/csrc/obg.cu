@@ -328,60 +328,6 @@ __device__ __forceinline__ void build_unit(const uint32_t (&w)[12], uint32_t* bi
   }
 }
 
-// Path-order leaf word m (codes 32m..32m+31) of the shared cube bitset:
-// 8 nibble gathers (see morton_word_from_cube), through the shared layout.
-template <int L>
-__device__ __forceinline__ uint32_t morton_word_from_smem(const uint32_t* s, uint32_t m) {
-  if constexpr (L == 1) {
-    return s[0] & 0xFFu;        // cube index == path code
-  } else {
-    const uint32_t base = code_to_cube(m << 5, L);
-    uint32_t out = 0;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const uint32_t g0 = c & 1, r0 = (c >> 1) & 1, g1 = (c >> 2) & 1;
-      const uint32_t idx = base + ((g0 | (g1 << 1)) << L) + (r0 << (2 * L));
-      const uint32_t nib = (s[Smem<L>::phys(idx >> 5)] >> (idx & 31u)) & 0xFu;
-      out |= ((nib & 3u) | ((nib & 12u) << 6)) << (g0 * 2 + r0 * 4 + g1 * 16);
-    }
-    return out;
-  }
-}
-
-// End of a CTA's segment of one tree: convert the shared cube bitset to the
-// tree's path-order pyramid in a shared scratch pyramid (leaf level, then each
-// interior level as the byte-wise OR of its children), OR its non-zero words
-// into `out` (zeroed by the host; several CTAs contribute to one tree) and
-// re-zero the cube for the next segment.  Replaces a workspace round trip +
-// separate pyramid kernel (ncu r4: 10.7 us + a 2 MB memset per build).
-template <int L>
-__device__ __forceinline__ void flush_pyramid(uint32_t* s, uint32_t* out) {
-  constexpr int64_t LW = level_words(L);
-  uint32_t* P = s + Smem<L>::words;                 // scratch pyramid, pyr_words(L) words
-  const int t = threadIdx.x;
-  __syncthreads();
-  for (int64_t m = t; m < LW; m += BUILD_BLOCK) P[level_offset(L) + m] = morton_word_from_smem<L>(s, uint32_t(m));
-  __syncthreads();
-  for (int i = t; i < Smem<L>::words; i += BUILD_BLOCK) s[i] = 0u;
-  for (int l = L - 1; l >= 1; --l) {
-    const int64_t off = level_offset(l), coff = level_offset(l + 1), cw = level_words(l + 1);
-    for (int64_t k = t; k < level_words(l); k += BUILD_BLOCK) {
-      uint32_t x = 0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (8 * k + q < cw) x |= nz4(P[coff + 8 * k + q]) << (4 * q);
-      P[off + k] = x;
-    }
-    __syncthreads();
-  }
-  for (int64_t i = t; i < pyr_words(L); i += BUILD_BLOCK) {
-    uint32_t x = P[i];
-    if (L == 1) x &= 0xFFu;
-    if (x) atomicOr(out + i, x);
-  }
-  __syncthreads();
-}
-
 template <int L, bool SMEM_BITS, bool COUNTS>
 __global__ void __launch_bounds__(BUILD_BLOCK, 2)
 k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t total_units,
@@ -418,7 +364,18 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
       build_unit<L, SMEM_BITS, COUNTS>(wa, bits, cnt, first);
       if (__any_sync(0xFFFFFFFFu, second)) build_unit<L, SMEM_BITS, COUNTS>(wb, bits, cnt, second);
     }
-    if constexpr (SMEM_BITS) flush_pyramid<L>(s_bits, out_pyr + tree * pyr_words(L));
+    if constexpr (SMEM_BITS) {
+      // OR the CTA's non-zero words into the tree's cube bitset.  (Converting
+      // to the path-order pyramid here instead costs 5.5x more: a tree spans
+      // ~4.6 CTA segments at C3 -- ncu r8.)
+      __syncthreads();
+      uint32_t* dst = ws + tree * CW;
+      for (int i = threadIdx.x; i < Smem<L>::words; i += BUILD_BLOCK) {
+        const uint32_t x = s_bits[i];
+        if (x) { atomicOr(dst + Smem<L>::canon(i), x); s_bits[i] = 0u; }   // pad words stay 0
+      }
+      __syncthreads();
+    }
     u = seg_end;
   }
 }
@@ -457,7 +414,7 @@ k_build_generic(const uint8_t* __restrict__ frames, int64_t n_pixels_used, int H
 //     per-level pyramids.  One CTA per (tree, chunk of <= 1024 leaf words).
 // ===========================================================================
 constexpr int PYR_BLOCK = 256;
-constexpr int PYR_CHUNK = 1024;  // leaf-level words per CTA (a 32x32x32 sub-cube)
+constexpr int PYR_CHUNK = 256;   // leaf-level words per CTA (a 16x16x32 sub-cube)
 
 // Leaf-level path-order word m (codes 32m..32m+31) from a cube bitset.
 // Codes of one word share all but bits 0..4 = b0 g0 r0 b1 g1; the (b1,b0)
@@ -491,13 +448,14 @@ k_pyramid(const uint32_t* __restrict__ src, int64_t src_stride, int L, uint32_t*
   uint32_t* o = out + tree * PW;
   // leaf level
   if (FROM_CUBE && L >= 5) {
-    // The chunk is the level-(L-5) node w0/1024: a 32x32x32 sub-cube whose
-    // 1024 (R', G') rows are one cube word each.  Stage them, then gather.
+    // The chunk's 8192 codes (low 13 code bits) form a 16x16x32 sub-cube
+    // (R' 4 bits, G' 4 bits, B' 5 bits) whose 256 (R', G') rows are one cube
+    // word each.  Stage them, then gather 8 nibbles per path-order word.
     const uint32_t cb = code_to_cube(uint32_t(w0) << 5, L);
     const uint32_t M = (1u << L) - 1u;
     const uint32_t Rb = (cb >> (2 * L)) & M, Gb = (cb >> L) & M, Bw = (cb & M) >> 5;
     for (int t = threadIdx.x; t < PYR_CHUNK; t += PYR_BLOCK) {
-      const uint32_t r = t >> 5, g = t & 31;
+      const uint32_t r = t >> 4, g = t & 15;
       s_c[t] = s[(int64_t(Rb + r) << (2 * L - 5)) | (int64_t(Gb + g) << (L - 5)) | Bw];
     }
     __syncthreads();
@@ -508,7 +466,7 @@ k_pyramid(const uint32_t* __restrict__ src, int64_t src_stride, int L, uint32_t*
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const uint32_t g0 = k & 1, r0 = (k >> 1) & 1, g1 = (k >> 2) & 1;
-        const uint32_t nib = (s_c[((rl + r0) << 5) + gl + g0 + 2 * g1] >> bl) & 0xFu;
+        const uint32_t nib = (s_c[((rl + r0) << 4) + gl + g0 + 2 * g1] >> bl) & 0xFu;
         x |= ((nib & 3u) | ((nib & 12u) << 6)) << (g0 * 2 + r0 * 4 + g1 * 16);
       }
       s_w[i] = x;
@@ -997,7 +955,7 @@ template <int L>
 static int launch_build_flat(const uint8_t* frames, int64_t units_per_frame, int64_t total_units, int group_size,
                              uint32_t* ws, uint32_t* out_pyr, uint32_t* counts, cudaStream_t st) {
   constexpr bool SMEM = L <= 6;
-  const size_t smem = SMEM ? size_t(Smem<L>::words + pyr_words(L)) * 4 : 0;   // cube + scratch pyramid
+  const size_t smem = SMEM ? size_t(Smem<L>::words) * 4 : 0;
   // one-time per instantiation: opt in to > 48 KB dynamic smem, cache occupancy
   static int occ[2] = {0, 0};
   int& blocks_per_sm = occ[counts ? 1 : 0];
@@ -1065,10 +1023,7 @@ int obg_build_presence(const uint8_t* frames, int n_frames, int height, int widt
   const int64_t P = int64_t(height) * width;
   const int64_t used_pixels = int64_t(n_groups) * group_size * P;
   const bool flat = n_regions == 1 && (P % 16) == 0 && (reinterpret_cast<uintptr_t>(frames) % 16) == 0;
-  // flat path with a shared-memory bitset (L <= 6) writes the pyramids
-  // directly; everything else goes through the cube workspace + k_pyramid
-  const bool direct = flat && levels <= 6;
-  if (!direct) CUDA_TRY(cudaMemsetAsync(ws, 0, size_t(n_trees * CW * 4), st));
+  CUDA_TRY(cudaMemsetAsync(ws, 0, size_t(n_trees * CW * 4), st));
   CUDA_TRY(cudaMemsetAsync(out_pyramids, 0, size_t(n_trees * PW * 4), st));
   if (out_counts) CUDA_TRY(cudaMemsetAsync(out_counts, 0, size_t(n_trees) * (size_t(1) << (3 * levels)) * 4, st));
   int rc = OBG_OK;
@@ -1095,7 +1050,6 @@ int obg_build_presence(const uint8_t* frames, int n_frames, int height, int widt
     LAUNCH_CHECK("k_build_generic");
   }
   if (rc != OBG_OK) return rc;
-  if (direct) return OBG_OK;
   return launch_pyramid(ws, CW, true, n_trees, levels, out_pyramids, st);
 }
 
