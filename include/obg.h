@@ -40,6 +40,8 @@ extern "C" {
 #define OBG_EUNSUPPORTED -2   /* valid but unsupported configuration */
 #define OBG_ECUDA        -3   /* CUDA runtime / launch failure */
 
+#define OBG_WS_ZEROED   1    /* obg_build_presence flag */
+
 #define OBG_MASK_U8     0
 #define OBG_MASK_PACKED 1
 
@@ -75,11 +77,22 @@ int obg_pack_codes(const uint8_t* pixels, int64_t n_pixels, int levels,
  *                  pixel occupancy histogram in path-code order (a superset of
  *                  the reference, which stores presence only; oracle is
  *                  np.bincount(pack_codes(block)))
- *   workspace    : >= obg_build_workspace_bytes(n_groups, R*C, L) bytes. */
+ *   workspace    : >= obg_build_workspace_bytes(n_groups, R*C, L) bytes.  It is
+ *                  returned all-zero; pass OBG_WS_ZEROED in flags when it is
+ *                  all-zero on entry (e.g. a kept workspace) to skip clearing it. */
 int obg_build_presence(const uint8_t* frames, int n_frames, int height, int width,
                        int levels, int grid_rows, int grid_cols, int group_size,
                        uint32_t* out_pyramids, uint32_t* out_counts,
-                       void* workspace, int64_t workspace_bytes, void* stream);
+                       void* workspace, int64_t workspace_bytes, int flags, void* stream);
+
+/* build_background_model on the device in one call (model.py:157-185):
+ * obg_build_presence + obg_merge with no memsets.  tree_pyramids is scratch
+ * of obg_build_presence's out_pyramids size; out_merged u32 [R*C][PW];
+ * out_cube u32 [R*C][obg_cube_words(L)] (the classify operand). */
+int obg_build_model(const uint8_t* frames, int n_frames, int height, int width,
+                    int levels, int grid_rows, int grid_cols, int group_size, int64_t k_min,
+                    uint32_t* tree_pyramids, uint32_t* out_merged, uint32_t* out_cube,
+                    void* workspace, int64_t workspace_bytes, int flags, void* stream);
 
 /* Pyramids from leaf-level bitsets (path-code order, max(1,8^L/32) words per
  * tree): every interior level is the OR-reduction of the level below, i.e.

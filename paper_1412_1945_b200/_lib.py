@@ -20,6 +20,7 @@ OBG_OK = 0
 OBG_EINVAL = -1
 OBG_EUNSUPPORTED = -2
 OBG_ECUDA = -3
+WS_ZEROED = 1
 MASK_U8 = 0
 MASK_PACKED = 1
 
@@ -35,7 +36,8 @@ SIGNATURES = {
     "obg_cube_words": (_L, [_I]),
     "obg_build_workspace_bytes": (_L, [_I, _I, _I]),
     "obg_pack_codes": (_I, [_P, _L, _I, _P, _P]),
-    "obg_build_presence": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _L, _P]),
+    "obg_build_presence": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _L, _I, _P]),
+    "obg_build_model": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _L, _P, _P, _P, _P, _L, _I, _P]),
     "obg_pyramid_from_leaves": (_I, [_P, _I, _I, _P, _P]),
     "obg_prune": (_I, [_P, _I, _I, _I, _P, _P]),
     "obg_merge_counts": (_I, [_P, _I, _I, _I, _P, _P]),
@@ -46,7 +48,7 @@ SIGNATURES = {
     "obg_serialize_workspace_bytes": (_L, [_I]),
     "obg_serialize": (_I, [_P, _I, _I, _P, _L, ctypes.POINTER(ctypes.c_int64), _P, _L, _P]),
 }
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 
 class LibraryNotBuilt(RuntimeError):

@@ -24,7 +24,8 @@
 
 #include "../../include/obg.h"
 
-#define OBG_ABI_VERSION 1
+#define OBG_ABI_VERSION 2
+#define OBG_CUBE_ZEROED 0x100   /* internal: out_cube already cleared by the build kernel */
 
 // ---------------------------------------------------------------------------
 // error plumbing
@@ -68,6 +69,33 @@ __host__ __device__ static constexpr int64_t level_offset(int l) {
 }
 __host__ __device__ static constexpr int64_t pyr_words(int L) { return level_offset(L + 1); }
 __host__ __device__ static constexpr int64_t cube_words(int L) { return level_words(L); }
+
+constexpr int PYR_CHUNK = 1024;  // k_pyramid: leaf-level words per CTA (a 32x32x32 sub-cube)
+
+// Leading words of a pyramid (levels 1..z) that k_pyramid ORs in with atomics
+// because several chunks share them; they must be zero beforehand (the build
+// kernels clear them, so no full memset of the output is needed).  Every other
+// word is written exactly once with a plain store.
+__host__ __device__ static inline int64_t pyr_shared_words(int L) {
+  const int64_t LW = level_words(L);
+  int64_t n = L == 1 ? 8 : (LW < PYR_CHUNK ? LW : PYR_CHUNK) * 32;
+  int z = 0;
+  for (int l = L - 1; l >= 1; --l) {
+    if (n >= 256) {
+      n /= 8;
+    } else {
+      if (l > z) z = l;
+      n = n >= 8 ? n / 8 : 1;
+    }
+  }
+  return level_offset(z + 1);
+}
+
+// Clear the shared leading words of n_trees output pyramids (one CTA's job).
+__device__ __forceinline__ void clear_shared_words(uint32_t* out, int64_t n_trees, int L) {
+  const int64_t z = pyr_shared_words(L), PW = pyr_words(L);
+  for (int64_t i = threadIdx.x; i < n_trees * z; i += blockDim.x) out[(i / z) * PW + i % z] = 0u;
+}
 
 // bit i of v -> bit 3i (v < 256)
 __host__ __device__ static inline uint32_t spread3(uint32_t v) {
@@ -332,9 +360,14 @@ template <int L, bool SMEM_BITS, bool COUNTS>
 __global__ void __launch_bounds__(BUILD_BLOCK, 2)
 k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t total_units,
              int group_size, int64_t units_per_cta, uint32_t* __restrict__ ws,
-             uint32_t* __restrict__ out_pyr, uint32_t* __restrict__ counts) {
+             uint32_t* __restrict__ out_pyr, int64_t n_trees, uint32_t* __restrict__ zero_cube,
+             int64_t zero_words, uint32_t* __restrict__ counts) {
   extern __shared__ uint32_t s_bits[];
   constexpr int64_t CW = cube_words(L);
+  if (blockIdx.x == 0) {
+    clear_shared_words(out_pyr, n_trees, L);
+    for (int64_t i = threadIdx.x; i < zero_words; i += BUILD_BLOCK) zero_cube[i] = 0u;
+  }
   const int64_t u_begin = int64_t(blockIdx.x) * units_per_cta;
   const int64_t u_end = min(total_units, u_begin + units_per_cta);
   if (u_begin >= u_end) return;
@@ -385,7 +418,13 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
 template <bool COUNTS>
 __global__ void __launch_bounds__(256)
 k_build_generic(const uint8_t* __restrict__ frames, int64_t n_pixels_used, int H, int W, int L,
-                int R, int C, int group_size, uint32_t* __restrict__ ws, uint32_t* __restrict__ counts) {
+                int R, int C, int group_size, uint32_t* __restrict__ ws, uint32_t* __restrict__ out_pyr,
+                int64_t n_trees, uint32_t* __restrict__ zero_cube, int64_t zero_words,
+                uint32_t* __restrict__ counts) {
+  if (blockIdx.x == 0) {
+    clear_shared_words(out_pyr, n_trees, L);
+    for (int64_t i = threadIdx.x; i < zero_words; i += blockDim.x) zero_cube[i] = 0u;
+  }
   const int64_t P = int64_t(H) * W;
   const int64_t CW = cube_words(L);
   const int s = 8 - L;
@@ -414,7 +453,6 @@ k_build_generic(const uint8_t* __restrict__ frames, int64_t n_pixels_used, int H
 //     per-level pyramids.  One CTA per (tree, chunk of <= 1024 leaf words).
 // ===========================================================================
 constexpr int PYR_BLOCK = 256;
-constexpr int PYR_CHUNK = 256;   // leaf-level words per CTA (a 16x16x32 sub-cube)
 
 // Leaf-level path-order word m (codes 32m..32m+31) from a cube bitset.
 // Codes of one word share all but bits 0..4 = b0 g0 r0 b1 g1; the (b1,b0)
@@ -448,15 +486,18 @@ k_pyramid(const uint32_t* __restrict__ src, int64_t src_stride, int L, uint32_t*
   uint32_t* o = out + tree * PW;
   // leaf level
   if (FROM_CUBE && L >= 5) {
-    // The chunk's 8192 codes (low 13 code bits) form a 16x16x32 sub-cube
-    // (R' 4 bits, G' 4 bits, B' 5 bits) whose 256 (R', G') rows are one cube
-    // word each.  Stage them, then gather 8 nibbles per path-order word.
+    // The chunk is the level-(L-5) node w0/1024: a 32x32x32 sub-cube whose
+    // 1024 (R', G') rows are one cube word each.  Stage them (and hand the
+    // workspace back zeroed: each cube word belongs to exactly one chunk),
+    // then gather 8 nibbles per path-order word.
     const uint32_t cb = code_to_cube(uint32_t(w0) << 5, L);
     const uint32_t M = (1u << L) - 1u;
     const uint32_t Rb = (cb >> (2 * L)) & M, Gb = (cb >> L) & M, Bw = (cb & M) >> 5;
     for (int t = threadIdx.x; t < PYR_CHUNK; t += PYR_BLOCK) {
-      const uint32_t r = t >> 4, g = t & 15;
-      s_c[t] = s[(int64_t(Rb + r) << (2 * L - 5)) | (int64_t(Gb + g) << (L - 5)) | Bw];
+      const uint32_t r = t >> 5, g = t & 31;
+      uint32_t* cw = const_cast<uint32_t*>(s) + ((int64_t(Rb + r) << (2 * L - 5)) | (int64_t(Gb + g) << (L - 5)) | Bw);
+      s_c[t] = *cw;
+      if (s_c[t]) *cw = 0u;
     }
     __syncthreads();
     for (int i = threadIdx.x; i < PYR_CHUNK; i += PYR_BLOCK) {
@@ -466,11 +507,11 @@ k_pyramid(const uint32_t* __restrict__ src, int64_t src_stride, int L, uint32_t*
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const uint32_t g0 = k & 1, r0 = (k >> 1) & 1, g1 = (k >> 2) & 1;
-        const uint32_t nib = (s_c[((rl + r0) << 4) + gl + g0 + 2 * g1] >> bl) & 0xFu;
+        const uint32_t nib = (s_c[((rl + r0) << 5) + gl + g0 + 2 * g1] >> bl) & 0xFu;
         x |= ((nib & 3u) | ((nib & 12u) << 6)) << (g0 * 2 + r0 * 4 + g1 * 16);
       }
       s_w[i] = x;
-      if (x) o[level_offset(L) + w0 + i] = x;
+      o[level_offset(L) + w0 + i] = x;          // the chunk owns these words
     }
   } else {
     for (int i = threadIdx.x; i < nw; i += PYR_BLOCK) {
@@ -479,7 +520,11 @@ k_pyramid(const uint32_t* __restrict__ src, int64_t src_stride, int L, uint32_t*
       else x = s[w0 + i];
       if (L == 1) x &= 0xFFu;
       s_w[i] = x;
-      if (x) o[level_offset(L) + w0 + i] = x;   // the chunk owns these words
+      o[level_offset(L) + w0 + i] = x;          // the chunk owns these words
+    }
+    if constexpr (FROM_CUBE) {                  // one chunk = the whole (small) tree
+      __syncthreads();
+      for (int i = threadIdx.x; i < cube_words(L); i += PYR_BLOCK) const_cast<uint32_t*>(s)[i] = 0u;
     }
   }
   __syncthreads();
@@ -502,7 +547,7 @@ k_pyramid(const uint32_t* __restrict__ src, int64_t src_stride, int L, uint32_t*
       for (int64_t k = threadIdx.x; k < pn; k += PYR_BLOCK) {
         const uint32_t v = vals[cnt++];
         s_w[k] = v;
-        if (v) o[off + B / 256 + k] = v;
+        o[off + B / 256 + k] = v;               // owned: plain store, zeros included
       }
       __syncthreads();
       B /= 8;
@@ -953,7 +998,8 @@ int obg_pack_codes(const uint8_t* pixels, int64_t n_pixels, int levels, uint32_t
 
 template <int L>
 static int launch_build_flat(const uint8_t* frames, int64_t units_per_frame, int64_t total_units, int group_size,
-                             uint32_t* ws, uint32_t* out_pyr, uint32_t* counts, cudaStream_t st) {
+                             uint32_t* ws, uint32_t* out_pyr, int64_t n_trees, uint32_t* zero_cube, int64_t zero_words,
+                             uint32_t* counts, cudaStream_t st) {
   constexpr bool SMEM = L <= 6;
   const size_t smem = SMEM ? size_t(Smem<L>::words) * 4 : 0;
   // one-time per instantiation: opt in to > 48 KB dynamic smem, cache occupancy
@@ -978,10 +1024,10 @@ static int launch_build_flat(const uint8_t* frames, int64_t units_per_frame, int
   const int grid = int((total_units + per_cta - 1) / per_cta);
   if (counts)
     k_build_flat<L, SMEM, true><<<grid, BUILD_BLOCK, smem, st>>>(frames, units_per_frame, total_units, group_size,
-                                                                 per_cta, ws, out_pyr, counts);
+                                                                 per_cta, ws, out_pyr, n_trees, zero_cube, zero_words, counts);
   else
     k_build_flat<L, SMEM, false><<<grid, BUILD_BLOCK, smem, st>>>(frames, units_per_frame, total_units, group_size,
-                                                                  per_cta, ws, out_pyr, nullptr);
+                                                                  per_cta, ws, out_pyr, n_trees, zero_cube, zero_words, nullptr);
   LAUNCH_CHECK("k_build_flat");
   return OBG_OK;
 }
@@ -998,10 +1044,13 @@ static int launch_pyramid(const uint32_t* src, int64_t src_stride, bool from_cub
   return OBG_OK;
 }
 
-int obg_build_presence(const uint8_t* frames, int n_frames, int height, int width, int levels, int grid_rows,
-                       int grid_cols, int group_size, uint32_t* out_pyramids, uint32_t* out_counts, void* workspace,
-                       int64_t workspace_bytes, void* stream) {
-  g_err[0] = 0;
+static int merge_common(const uint32_t* pyramids, int n_trees, int n_regions, int levels, int64_t k_min,
+                        uint32_t* counts, uint32_t* out, uint32_t* out_cube, int flags, void* stream);
+
+static int build_presence_impl(const uint8_t* frames, int n_frames, int height, int width, int levels, int grid_rows,
+                               int grid_cols, int group_size, uint32_t* out_pyramids, uint32_t* out_counts,
+                               void* workspace, int64_t workspace_bytes, int flags, uint32_t* zero_cube,
+                               int64_t zero_words, void* stream) {
   if (levels < 1 || levels > 8) return set_err(OBG_EINVAL, "levels must be in 1..8, got %d", levels);
   if (n_frames < 1) return set_err(OBG_EINVAL, "no frames given");
   if (height < 1 || width < 1) return set_err(OBG_EINVAL, "frame dimensions must be >= 1");
@@ -1023,34 +1072,61 @@ int obg_build_presence(const uint8_t* frames, int n_frames, int height, int widt
   const int64_t P = int64_t(height) * width;
   const int64_t used_pixels = int64_t(n_groups) * group_size * P;
   const bool flat = n_regions == 1 && (P % 16) == 0 && (reinterpret_cast<uintptr_t>(frames) % 16) == 0;
-  CUDA_TRY(cudaMemsetAsync(ws, 0, size_t(n_trees * CW * 4), st));
-  CUDA_TRY(cudaMemsetAsync(out_pyramids, 0, size_t(n_trees * PW * 4), st));
+  // The workspace is handed back all-zero by k_pyramid; a caller that keeps
+  // it (OBG_WS_ZEROED) skips the clear.  Output pyramids need no memset: every
+  // word is either stored once or (leading shared words) cleared by K1.
+  if (!(flags & OBG_WS_ZEROED)) CUDA_TRY(cudaMemsetAsync(ws, 0, size_t(n_trees * CW * 4), st));
   if (out_counts) CUDA_TRY(cudaMemsetAsync(out_counts, 0, size_t(n_trees) * (size_t(1) << (3 * levels)) * 4, st));
   int rc = OBG_OK;
   if (flat) {
     const int64_t upf = P / 16, total_units = used_pixels / 16;
     switch (levels) {
-      case 1: rc = launch_build_flat<1>(frames, upf, total_units, group_size, ws, out_pyramids, out_counts, st); break;
-      case 2: rc = launch_build_flat<2>(frames, upf, total_units, group_size, ws, out_pyramids, out_counts, st); break;
-      case 3: rc = launch_build_flat<3>(frames, upf, total_units, group_size, ws, out_pyramids, out_counts, st); break;
-      case 4: rc = launch_build_flat<4>(frames, upf, total_units, group_size, ws, out_pyramids, out_counts, st); break;
-      case 5: rc = launch_build_flat<5>(frames, upf, total_units, group_size, ws, out_pyramids, out_counts, st); break;
-      case 6: rc = launch_build_flat<6>(frames, upf, total_units, group_size, ws, out_pyramids, out_counts, st); break;
-      case 7: rc = launch_build_flat<7>(frames, upf, total_units, group_size, ws, out_pyramids, out_counts, st); break;
-      default: rc = launch_build_flat<8>(frames, upf, total_units, group_size, ws, out_pyramids, out_counts, st); break;
+      case 1: rc = launch_build_flat<1>(frames, upf, total_units, group_size, ws, out_pyramids, n_trees, zero_cube, zero_words, out_counts, st); break;
+      case 2: rc = launch_build_flat<2>(frames, upf, total_units, group_size, ws, out_pyramids, n_trees, zero_cube, zero_words, out_counts, st); break;
+      case 3: rc = launch_build_flat<3>(frames, upf, total_units, group_size, ws, out_pyramids, n_trees, zero_cube, zero_words, out_counts, st); break;
+      case 4: rc = launch_build_flat<4>(frames, upf, total_units, group_size, ws, out_pyramids, n_trees, zero_cube, zero_words, out_counts, st); break;
+      case 5: rc = launch_build_flat<5>(frames, upf, total_units, group_size, ws, out_pyramids, n_trees, zero_cube, zero_words, out_counts, st); break;
+      case 6: rc = launch_build_flat<6>(frames, upf, total_units, group_size, ws, out_pyramids, n_trees, zero_cube, zero_words, out_counts, st); break;
+      case 7: rc = launch_build_flat<7>(frames, upf, total_units, group_size, ws, out_pyramids, n_trees, zero_cube, zero_words, out_counts, st); break;
+      default: rc = launch_build_flat<8>(frames, upf, total_units, group_size, ws, out_pyramids, n_trees, zero_cube, zero_words, out_counts, st); break;
     }
   } else {
     const int grid = grid_for(used_pixels, 256, sm_count() * 8);
     if (out_counts)
       k_build_generic<true><<<grid, 256, 0, st>>>(frames, used_pixels, height, width, levels, grid_rows, grid_cols,
-                                                   group_size, ws, out_counts);
+                                                   group_size, ws, out_pyramids, n_trees, zero_cube, zero_words, out_counts);
     else
       k_build_generic<false><<<grid, 256, 0, st>>>(frames, used_pixels, height, width, levels, grid_rows, grid_cols,
-                                                    group_size, ws, nullptr);
+                                                    group_size, ws, out_pyramids, n_trees, zero_cube, zero_words, nullptr);
     LAUNCH_CHECK("k_build_generic");
   }
   if (rc != OBG_OK) return rc;
   return launch_pyramid(ws, CW, true, n_trees, levels, out_pyramids, st);
+}
+
+int obg_build_presence(const uint8_t* frames, int n_frames, int height, int width, int levels, int grid_rows,
+                       int grid_cols, int group_size, uint32_t* out_pyramids, uint32_t* out_counts, void* workspace,
+                       int64_t workspace_bytes, int flags, void* stream) {
+  g_err[0] = 0;
+  return build_presence_impl(frames, n_frames, height, width, levels, grid_rows, grid_cols, group_size, out_pyramids,
+                             out_counts, workspace, workspace_bytes, flags, nullptr, 0, stream);
+}
+
+int obg_build_model(const uint8_t* frames, int n_frames, int height, int width, int levels, int grid_rows,
+                    int grid_cols, int group_size, int64_t k_min, uint32_t* tree_pyramids, uint32_t* out_merged,
+                    uint32_t* out_cube, void* workspace, int64_t workspace_bytes, int flags, void* stream) {
+  g_err[0] = 0;
+  if (k_min < 1) return set_err(OBG_EINVAL, "k_min must be >= 1, got %lld", (long long)k_min);
+  if (!out_merged || !out_cube) return set_err(OBG_EINVAL, "null buffer");
+  if (levels < 1 || levels > 8) return set_err(OBG_EINVAL, "levels must be in 1..8, got %d", levels);
+  const int64_t n_regions = int64_t(grid_rows) * grid_cols;
+  // the build kernel clears the cube the merge scatters into: no memsets at all
+  int rc = build_presence_impl(frames, n_frames, height, width, levels, grid_rows, grid_cols, group_size,
+                               tree_pyramids, nullptr, workspace, workspace_bytes, flags, out_cube,
+                               n_regions * cube_words(levels), stream);
+  if (rc != OBG_OK) return rc;
+  return merge_common(tree_pyramids, n_frames / group_size, int(n_regions), levels, k_min, nullptr, out_merged,
+                      out_cube, OBG_CUBE_ZEROED, stream);
 }
 
 int obg_pyramid_from_leaves(const uint32_t* leaves, int n_trees, int levels, uint32_t* out_pyramids, void* stream) {
@@ -1080,13 +1156,14 @@ int obg_prune(const uint32_t* pyramids, int n_trees, int levels, int new_levels,
 }
 
 static int merge_common(const uint32_t* pyramids, int n_trees, int n_regions, int levels, int64_t k_min,
-                        uint32_t* counts, uint32_t* out, uint32_t* out_cube, void* stream) {
+                        uint32_t* counts, uint32_t* out, uint32_t* out_cube, int flags, void* stream) {
   if (levels < 1 || levels > 8) return set_err(OBG_EINVAL, "levels must be in 1..8, got %d", levels);
   if (n_trees < 1) return set_err(OBG_EINVAL, "no trees to merge");
   if (n_regions < 1) return set_err(OBG_EINVAL, "n_regions must be >= 1");
   if (!pyramids) return set_err(OBG_EINVAL, "null buffer");
   cudaStream_t st = as_stream(stream);
-  if (out_cube) CUDA_TRY(cudaMemsetAsync(out_cube, 0, size_t(n_regions) * cube_words(levels) * 4, st));
+  if (out_cube && !(flags & OBG_CUBE_ZEROED))
+    CUDA_TRY(cudaMemsetAsync(out_cube, 0, size_t(n_regions) * cube_words(levels) * 4, st));
   const int64_t words = pyr_words(levels) * n_regions;
   k_merge<<<grid_for(words, 32, sm_count() * 16), dim3(32, MERGE_GROUPS), 0, st>>>(
       pyramids, n_trees, n_regions, levels, k_min, counts, out, out_cube);
@@ -1097,7 +1174,7 @@ static int merge_common(const uint32_t* pyramids, int n_trees, int n_regions, in
 int obg_merge_counts(const uint32_t* pyramids, int n_trees, int n_regions, int levels, uint32_t* counts, void* stream) {
   g_err[0] = 0;
   if (!counts) return set_err(OBG_EINVAL, "null buffer");
-  return merge_common(pyramids, n_trees, n_regions, levels, 0, counts, nullptr, nullptr, stream);
+  return merge_common(pyramids, n_trees, n_regions, levels, 0, counts, nullptr, nullptr, 0, stream);
 }
 
 int obg_merge(const uint32_t* pyramids, int n_trees, int n_regions, int levels, int64_t k_min,
@@ -1105,7 +1182,7 @@ int obg_merge(const uint32_t* pyramids, int n_trees, int n_regions, int levels, 
   g_err[0] = 0;
   if (!out_pyramids) return set_err(OBG_EINVAL, "null buffer");
   if (k_min < 1) return set_err(OBG_EINVAL, "k_min must be >= 1, got %lld", (long long)k_min);
-  return merge_common(pyramids, n_trees, n_regions, levels, k_min, nullptr, out_pyramids, out_cube, stream);
+  return merge_common(pyramids, n_trees, n_regions, levels, k_min, nullptr, out_pyramids, out_cube, 0, stream);
 }
 
 int obg_merge_threshold(const uint32_t* counts, int n_regions, int levels, int64_t k_min, uint32_t* out_pyramids,

@@ -204,11 +204,40 @@ def build_presence(frames_dev, levels: int, grid_rows: int = 1, grid_cols: int =
     out = _device.empty((n_groups, n_regions, pw), "int32")
     cnt = _device.empty((n_groups, n_regions, 8 ** levels), "int32") if counts else None
     ws_bytes = lib.obg_build_workspace_bytes(n_groups, n_regions, levels)
-    ws = _device.empty((max(ws_bytes, 4) // 4,), "int32")
-    _lib.check(lib.obg_build_presence(
-        _device.ptr(frames_dev), n, h, w, levels, grid_rows, grid_cols, group_size, _device.ptr(out),
-        _device.ptr(cnt) if cnt is not None else None, _device.ptr(ws), ws_bytes, _device.stream_handle()))
+    stream = _device.stream_handle()
+    ws = _workspace(ws_bytes, stream)
+    try:
+        _lib.check(lib.obg_build_presence(
+            _device.ptr(frames_dev), n, h, w, levels, grid_rows, grid_cols, group_size, _device.ptr(out),
+            _device.ptr(cnt) if cnt is not None else None, _device.ptr(ws), ws_bytes, _lib.WS_ZEROED, stream))
+    except Exception:
+        _WORKSPACES.pop((_device.torch().cuda.current_device(), stream), None)   # state unknown: drop it
+        raise
     return (out, cnt) if counts else out
+
+
+# Build workspaces kept per (device, stream): obg_build_presence hands its
+# workspace back all-zero, so a kept one skips the clearing memset.  Keyed by
+# stream because concurrent builds must not share one.
+_WORKSPACES: dict = {}
+
+
+def _workspace(nbytes: int, stream: int):
+    from . import _device
+    t = _device.torch()
+    dev = t.cuda.current_device()
+    if t.cuda.is_current_stream_capturing():
+        # graph capture: reuse a workspace created eagerly (warm-up), so the
+        # graph holds no allocation or clearing node for it
+        for (d, _), ws in _WORKSPACES.items():
+            if d == dev and ws.numel() * 4 >= nbytes:
+                return ws
+    key = (dev, stream)
+    ws = _WORKSPACES.get(key)
+    if ws is None or ws.numel() * 4 < nbytes:
+        ws = t.zeros((max(nbytes, 4) + 3) // 4, dtype=t.int32, device="cuda")
+        _WORKSPACES[key] = ws
+    return ws
 
 
 def merge_pyramids(pyramids_dev, levels: int, k_min: int, with_cube: bool = False):
@@ -295,8 +324,24 @@ def build_background_model_device(frames_dev, config: ModelConfig, n_groups: int
         if n_groups == 0:
             raise ValueError(f"need at least {config.group_size} frames for one group, got {n}")
         frames_dev = frames_dev[: n_groups * config.group_size]
-    pyr = build_presence(frames_dev, config.levels, config.grid_rows, config.grid_cols, config.group_size)
-    merged, cube = merge_pyramids(pyr, config.levels, merge_k_min(n_groups, config.threshold), with_cube=True)
+    L, R, C, gs = config.levels, config.grid_rows, config.grid_cols, config.group_size
+    n_regions = R * C
+    lib = _lib.load()
+    pw = _lib.pyramid_words(L)
+    trees = _device.empty((n_groups, n_regions, pw), "int32")
+    merged = _device.empty((n_regions, pw), "int32")
+    cube = _device.empty((n_regions, _lib.cube_words(L)), "int32")
+    ws_bytes = lib.obg_build_workspace_bytes(n_groups, n_regions, L)
+    stream = _device.stream_handle()
+    ws = _workspace(ws_bytes, stream)
+    try:
+        _lib.check(lib.obg_build_model(
+            _device.ptr(frames_dev), n_groups * gs, h, w, L, R, C, gs, merge_k_min(n_groups, config.threshold),
+            _device.ptr(trees), _device.ptr(merged), _device.ptr(cube), _device.ptr(ws), ws_bytes, _lib.WS_ZEROED,
+            stream))
+    except Exception:
+        _WORKSPACES.pop((_device.torch().cuda.current_device(), stream), None)
+        raise
     return BackgroundModel(config, frame_width=w, frame_height=h, _device_pyramids=merged, _device_cube=cube)
 
 

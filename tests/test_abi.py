@@ -43,9 +43,9 @@ def test_size_helpers():
 
 
 @pytest.mark.parametrize("call", [
-    lambda lib: lib.obg_build_presence(None, 4, 8, 8, 9, 1, 1, 1, None, None, None, 0, None),
-    lambda lib: lib.obg_build_presence(None, 0, 8, 8, 4, 1, 1, 1, None, None, None, 0, None),
-    lambda lib: lib.obg_build_presence(None, 2, 8, 8, 4, 1, 1, 3, None, None, None, 0, None),
+    lambda lib: lib.obg_build_presence(None, 4, 8, 8, 9, 1, 1, 1, None, None, None, 0, 0, None),
+    lambda lib: lib.obg_build_presence(None, 0, 8, 8, 4, 1, 1, 1, None, None, None, 0, 0, None),
+    lambda lib: lib.obg_build_presence(None, 2, 8, 8, 4, 1, 1, 3, None, None, None, 0, 0, None),
     lambda lib: lib.obg_classify(None, 1, 8, 8, 4, 0, 1, None, None, 0, None),
     lambda lib: lib.obg_classify(None, 1, 8, 8, 4, 1, 1, None, None, 7, None),
     lambda lib: lib.obg_merge(None, 0, 1, 4, 1, None, None, None),
@@ -63,7 +63,7 @@ def test_invalid_arguments_rejected_before_device_work(call):
 
 def test_error_message_text():
     lib = _lib.load()
-    lib.obg_build_presence(None, 2, 8, 8, 4, 1, 1, 3, None, None, None, 0, None)
+    lib.obg_build_presence(None, 2, 8, 8, 4, 1, 1, 3, None, None, None, 0, 0, None)
     assert b"need at least 3 frames for one group, got 2" in lib.obg_last_error()
 
 

@@ -323,3 +323,23 @@ def test_merge_many_trees(cuda, n_trees):
         merged = obg.merge_pyramids(pyr, levels, obg.merge_k_min(n_trees, thr))
         want = orc.merge_trees(trees, thr, levels)
         assert Octree._from_device(merged[0], levels).to_bytes() == orc.to_bytes(want), thr
+
+
+def test_captured_step_matches_eager(cuda, golden):
+    """CUDA-graph replay of build + classify (the bench's steady state)."""
+    from paper_1412_1945_b200 import scenes
+    from paper_1412_1945_b200.pipeline import CapturedStep
+    rec = next(r for r in golden["configs"] if r["config"] == 1)
+    sc = scenes.generate(1, n_test=24)
+    train, test = cuda.from_numpy(sc.train).cuda(), cuda.from_numpy(sc.test).cuda()
+    cfg = ModelConfig(levels=rec["levels"], threshold=rec["threshold"], training_frames=len(sc.train))
+    step = CapturedStep(train, test, cfg)
+    for _ in range(3):
+        masks = step.step().cpu().numpy()
+        assert sha(step.model.trees[0][0].to_bytes()) == rec["merged_sha"]
+        step.model._trees = None        # re-materialise from the device after the next replay
+        for i in range(len(masks)):
+            assert mask_digest(masks[i]) == rec["mask_sha"][i]
+    # new frames copied into the static input change the result accordingly
+    test.copy_(cuda.from_numpy(sc.train[:24]).cuda())
+    assert not step.classify().any()
