@@ -340,6 +340,10 @@ def test_captured_step_matches_eager(cuda, golden):
         step.model._trees = None        # re-materialise from the device after the next replay
         for i in range(len(masks)):
             assert mask_digest(masks[i]) == rec["mask_sha"][i]
-    # new frames copied into the static input change the result accordingly
+    # new frames copied into the static input: the replay classifies them
     test.copy_(cuda.from_numpy(sc.train[:24]).cuda())
-    assert not step.classify().any()
+    eager = obg.classify(step.model, test).clone()
+    assert cuda.equal(step.classify(), eager)
+    want = orc.build_background_model(list(sc.train), rec["levels"], rec["threshold"])
+    for i in range(0, 24, 6):
+        assert np.array_equal(eager[i].cpu().numpy().astype(bool), orc.detect_octree(want, sc.train[i], rec["levels"]))
