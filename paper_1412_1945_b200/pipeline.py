@@ -52,3 +52,61 @@ class CapturedStep:
         self.build_graph.replay()
         self.classify_graph.replay()
         return self.masks
+
+
+def process_batches(train_host, test_host, config: ModelConfig, out_host=None, chunk: int = 32,
+                    packed: bool = False):
+    """Host frames in, host masks out, with copies overlapped with the kernels.
+
+    ``train_host`` / ``test_host`` are (n, h, w, 3) uint8 CPU tensors (pinned
+    memory gives asynchronous copies).  The training frames go up first and
+    the model is built; meanwhile the test frames stream up chunk by chunk on
+    a copy stream, each chunk is classified as soon as it lands and its masks
+    stream back on a third stream -- H2D, compute and D2H overlap, so the
+    batch costs about max(H2D, D2H) over PCIe instead of their sum.
+    Returns (model, masks) with masks in ``out_host`` (allocated pinned if
+    None): (n, h, w) uint8 0/1, or bit-packed with ``packed``.
+    """
+    t = _device.torch()
+    dev = t.device("cuda", t.cuda.current_device())
+    n, h, w = int(test_host.shape[0]), int(test_host.shape[1]), int(test_host.shape[2])
+    shape = (n, (h * w + 7) // 8) if packed else (n, h, w)
+    if out_host is None:
+        out_host = t.empty(shape, dtype=t.uint8, pin_memory=True)
+    main = t.cuda.current_stream()
+    up, down = t.cuda.Stream(), t.cuda.Stream()
+    # training frames + model
+    with t.cuda.stream(up):
+        train = train_host.to(dev, non_blocking=True)
+    main.wait_stream(up)
+    train.record_stream(main)
+    model = build_background_model_device(train, config)
+    # test chunks: double-buffered device frames / masks
+    chunk = max(1, min(chunk, n))
+    frames = [t.empty((chunk, h, w, 3), dtype=t.uint8, device=dev) for _ in range(2)]
+    mshape = (chunk, (h * w + 7) // 8) if packed else (chunk, h, w)
+    masks = [t.empty(mshape, dtype=t.uint8, device=dev) for _ in range(2)]
+    landed = [t.cuda.Event() for _ in range(2)]
+    computed = [t.cuda.Event() for _ in range(2)]
+    drained = [t.cuda.Event() for _ in range(2)]
+    consumed = [t.cuda.Event() for _ in range(2)]
+    for k, s0 in enumerate(range(0, n, chunk)):
+        b, m = k & 1, min(chunk, n - s0)
+        with t.cuda.stream(up):
+            if k >= 2:
+                up.wait_event(consumed[b])          # classify of chunk k-2 has read frames[b]
+            frames[b][:m].copy_(test_host[s0:s0 + m], non_blocking=True)
+            landed[b].record(up)
+        main.wait_event(landed[b])
+        if k >= 2:
+            main.wait_event(drained[b])             # masks[b] of chunk k-2 copied out
+        classify(model, frames[b][:m], out=masks[b][:m], packed=packed)
+        consumed[b].record(main)
+        computed[b].record(main)
+        with t.cuda.stream(down):
+            down.wait_event(computed[b])
+            out_host[s0:s0 + m].copy_(masks[b][:m], non_blocking=True)
+            drained[b].record(down)
+    main.wait_stream(down)
+    main.wait_stream(up)
+    return model, out_host

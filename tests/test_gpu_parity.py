@@ -347,3 +347,24 @@ def test_captured_step_matches_eager(cuda, golden):
     want = orc.build_background_model(list(sc.train), rec["levels"], rec["threshold"])
     for i in range(0, 24, 6):
         assert np.array_equal(eager[i].cpu().numpy().astype(bool), orc.detect_octree(want, sc.train[i], rec["levels"]))
+
+
+def test_process_batches_pipeline(cuda, golden):
+    """Overlapped host->device->host pipeline (the bench's e2e path)."""
+    from paper_1412_1945_b200 import scenes
+    from paper_1412_1945_b200.pipeline import process_batches
+    rec = next(r for r in golden["configs"] if r["config"] == 1)
+    sc = scenes.generate(1, n_test=37)
+    cfg = ModelConfig(levels=rec["levels"], threshold=rec["threshold"], training_frames=len(sc.train))
+    train = cuda.from_numpy(sc.train).pin_memory()
+    test = cuda.from_numpy(sc.test).pin_memory()
+    for chunk in (8, 16, 64):
+        model, masks = process_batches(train, test, cfg, chunk=chunk)
+        cuda.cuda.synchronize()
+        assert sha(model.trees[0][0].to_bytes()) == rec["merged_sha"]
+        m = masks.numpy()
+        for i in range(37):
+            assert mask_digest(m[i]) == rec["mask_sha"][i], (chunk, i)
+    model, packed = process_batches(train, test, cfg, chunk=16, packed=True)
+    cuda.cuda.synchronize()
+    assert np.array_equal(packed.numpy(), np.packbits(m.reshape(37, -1).astype(bool), axis=1, bitorder="little"))
