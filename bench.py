@@ -383,6 +383,13 @@ def run_ours(args):
                        if world == 1 else "eager H2D + sharded build + classify + D2H"}
 
     peak, peak_src = peaks()
+    traffic = None
+    try:   # dram read+write of the classify kernel from the committed ncu --set full capture
+        with open(os.path.join(REPO, "profiles", "traffic.json")) as f:
+            tj = json.load(f)
+        traffic = int(tj["dram_bytes_read"] + tj["dram_bytes_write"])
+    except Exception:
+        pass
     cls_bytes = n_test * P * 4                 # 3 B read + 1 B mask written per pixel
     build_bytes = n_train * (P * 3 + obg._lib.cube_words(cfg.levels) * 4)
     cls_gbs = cls_bytes / (cls_avg / 1000) / 1e9
@@ -412,7 +419,8 @@ def run_ours(args):
                        "build_hbm_frac": round(build_gbs / peak, 4)},
             "roofline": {"bound": "hbm", "kernel": "k_classify_flat<6> (obg_classify)",
                          "achieved": round(cls_gbs, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(cls_gbs / peak, 4), "traffic": None, "peak_source": peak_src,
+                         "frac": round(cls_gbs / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                         "traffic_source": "profiles/traffic.json (ncu --set full, bytes per launch)",
                          "algorithmic_bytes_per_launch": cls_bytes,
                          "bytes_per_unit": "4 B/px (3 read + 1 mask byte written) x 256 x 1920x1080"},
             "cpu_baseline": cpu,
