@@ -254,9 +254,17 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # OBG_BENCH_DEVICE / OBG_BENCH_BACKEND exist only to exercise the
+    # multi-rank path on a single GPU (gloo moves the all-reduce to the host,
+    # so co-located ranks never wait on each other inside a kernel).
+    local = int(os.environ.get("OBG_BENCH_DEVICE", local))
+    backend = os.environ.get("OBG_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
 
     # weak scaling: every rank gets its own seeded scene shard
