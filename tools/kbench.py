@@ -1,0 +1,68 @@
+"""Micro-benchmark of individual kernels on synthetic inputs (CUDA events).
+
+    python tools/kbench.py build|classify [--frames N] [--scene c3|const|repeat|uniform] [--levels L]
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1412_1945_b200 as obg  # noqa: E402
+from paper_1412_1945_b200 import scenes  # noqa: E402
+
+
+def frames_for(kind, n, levels):
+    if kind == "c3":
+        return scenes.generate(3, n_train=n, n_test=0).train
+    if kind == "const":
+        f = np.empty((n, 1080, 1920, 3), np.uint8)
+        f[...] = (90, 140, 60)
+        return f
+    if kind == "repeat":
+        one = scenes.generate(3, n_train=1, n_test=0).train
+        return np.repeat(one, n, axis=0)
+    if kind == "uniform":
+        return np.random.default_rng(0).integers(0, 256, size=(n, 1080, 1920, 3), dtype=np.uint8)
+    raise SystemExit(kind)
+
+
+def timeit(fn, reps=20):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("what", choices=["build", "classify", "model"])
+    ap.add_argument("--frames", type=int, default=64)
+    ap.add_argument("--scene", default="c3")
+    ap.add_argument("--levels", type=int, default=6)
+    a = ap.parse_args()
+    f = torch.from_numpy(frames_for(a.scene, a.frames, a.levels)).cuda()
+    px = f.shape[0] * f.shape[1] * f.shape[2]
+    cfg = obg.ModelConfig(levels=a.levels, threshold=0.5, training_frames=a.frames)
+    if a.what == "build":
+        ms = timeit(lambda: obg.build_presence(f, a.levels))
+    elif a.what == "model":
+        ms = timeit(lambda: obg.build_background_model_device(f, cfg))
+    else:
+        model = obg.build_background_model_device(f, cfg)
+        out = torch.empty(f.shape[:3], dtype=torch.uint8, device="cuda")
+        ms = timeit(lambda: obg.classify(model, f, out=out))
+    print(f"{a.what} scene={a.scene} L={a.levels} frames={a.frames}: {ms * 1000:.1f} us, "
+          f"{px / ms / 1e6:.1f} Gpx/s, {px * (3 if a.what != 'classify' else 4) / ms / 1e6:.1f} GB/s")
+
+
+if __name__ == "__main__":
+    main()
