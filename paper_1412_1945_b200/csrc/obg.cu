@@ -172,13 +172,15 @@ struct Smem {
 };
 
 // Skewed-layout byte address and bit selector of pixel x = [*, G, B, R].
+// `obase` (optional) is a shared-window base with its low 9 bits clear: it is
+// OR-ed into the in-row offset at no cost instead of a separate add.
 template <int L>
-__device__ __forceinline__ void skew_lookup(uint32_t x, uint32_t& addr, uint32_t& bsel) {
+__device__ __forceinline__ void skew_lookup(uint32_t x, uint32_t& addr, uint32_t& bsel, uint32_t obase = 0) {
   constexpr int s = 8 - L;
   const uint32_t r = __umulhi(x, 1u << (8 - s));                    // x >> (24+s) = R'
   bsel = __umulhi(x, 1u << (16 - s));                               // x >> (16+s): low 5 bits = B' & 31
   const uint32_t g = __umulhi(x, 1u << (13 + 2 * L));               // x >> (19-2L): G' at bit L-3
-  uint32_t c = g & (((1u << L) - 1u) << (L - 3));
+  uint32_t c = (g & (((1u << L) - 1u) << (L - 3))) | obase;
   if constexpr (L == 6) c |= __umulhi(x, 1u << (5 + L)) & 4u;        // x >> (27-L): B'5 at bit 2
   addr = r * (Smem<L>::ROWW * 4u) + c;
 }
@@ -297,12 +299,12 @@ __device__ __forceinline__ uint32_t operand_to_cube(uint32_t x) {
 // Word byte address + bit selector of operand x in the leaf bitset `bits`
 // (shared for L <= 6, global cube for L >= 7).
 template <int L>
-__device__ __forceinline__ void bit_position(uint32_t x, uint32_t& addr, uint32_t& bsel) {
+__device__ __forceinline__ void bit_position(uint32_t x, uint32_t& addr, uint32_t& bsel, uint32_t obase = 0) {
   if constexpr (Smem<L>::skew) {
-    skew_lookup<L>(x, addr, bsel);
+    skew_lookup<L>(x, addr, bsel, obase);
   } else {
     const uint32_t idx = cube_idx<L>(x);
-    addr = (idx >> 5) << 2;
+    addr = ((idx >> 5) << 2) + obase;
     bsel = idx;
   }
 }
@@ -319,33 +321,45 @@ __device__ __forceinline__ void unpack16(const uint32_t (&w)[12], uint32_t (&px)
 // warp-uniform branch, so the common path has no divergence (ncu r4-r6:
 // per-pixel divergent branches cost ~5 instructions/pixel).  About 0.45 % of
 // pixels miss at C3 (first occurrences of a colour within a CTA's range).
-__device__ __forceinline__ uint32_t* dyn_smem() {
-  extern __shared__ uint32_t s_dyn[];
-  return s_dyn;
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void reds_or(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.or.b32 [%0], %1;" :: "r"(a), "r"(v) : "memory");
 }
 
+// `sbase` = 32-bit shared-window address of the static, 1 KB-aligned bitset,
+// merged into the lookup address by bit_position (no per-pixel add);
+// `bits` = global bitset for L >= 7.
 template <int L, bool SMEM_BITS, bool COUNTS>
-__device__ __forceinline__ void build_unit(const uint32_t (&w)[12], uint32_t* bits, uint32_t* cnt, bool valid) {
+__device__ __forceinline__ void build_unit(const uint32_t (&w)[12], uint32_t* bits, uint32_t sbase, uint32_t* cnt,
+                                           bool valid) {
   uint32_t px[16];
   unpack16<0, L>(w, px);
-  // the shared window base is known statically; lets ptxas fold it into LDS
-  char* base = SMEM_BITS ? reinterpret_cast<char*>(dyn_smem()) : reinterpret_cast<char*>(bits);
+  char* base = reinterpret_cast<char*>(bits);
 #pragma unroll
   for (int g = 0; g < 16; g += 4) {
     uint32_t addr[4], bsel[4], v[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       uint32_t wd;
-      bit_position<L>(px[g + j], addr[j], bsel[j]);
-      if constexpr (SMEM_BITS) wd = *reinterpret_cast<const uint32_t*>(base + addr[j]);
+      bit_position<L>(px[g + j], addr[j], bsel[j], SMEM_BITS ? sbase : 0u);
+      if constexpr (SMEM_BITS) wd = lds_u32(addr[j]);
       else wd = *reinterpret_cast<volatile uint32_t*>(base + addr[j]);
       v[j] = __funnelshift_r(wd, wd, bsel[j]);
     }
     const bool miss = valid && !(v[0] & v[1] & v[2] & v[3] & 1u);
     if (__any_sync(0xFFFFFFFFu, miss)) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (valid && !(v[j] & 1u)) atomicOr(reinterpret_cast<uint32_t*>(base + addr[j]), 1u << (bsel[j] & 31u));
+      for (int j = 0; j < 4; ++j) {
+        if (valid && !(v[j] & 1u)) {
+          if constexpr (SMEM_BITS) reds_or(addr[j], 1u << (bsel[j] & 31u));
+          else atomicOr(reinterpret_cast<uint32_t*>(base + addr[j]), 1u << (bsel[j] & 31u));
+        }
+      }
     }
   }
   if constexpr (COUNTS) {
@@ -362,7 +376,10 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
              int group_size, int64_t units_per_cta, uint32_t* __restrict__ ws,
              uint32_t* __restrict__ out_pyr, int64_t n_trees, uint32_t* __restrict__ zero_cube,
              int64_t zero_words, uint32_t* __restrict__ counts) {
-  extern __shared__ uint32_t s_bits[];
+  // static shared array: its address is a compile-time constant, so the
+  // lookups and atomics use [reg + imm] addressing (no per-pixel base add)
+  __shared__ __align__(1024) uint32_t s_bits[SMEM_BITS ? Smem<L>::words : 1];
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(s_bits));
   constexpr int64_t CW = cube_words(L);
   if (blockIdx.x == 0) {
     clear_shared_words(out_pyr, n_trees, L);
@@ -394,8 +411,8 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
       uint32_t wa[12], wb[12];
       if (first) load_unit(frames, v, wa);
       if (second) load_unit(frames, v + BUILD_BLOCK, wb);
-      build_unit<L, SMEM_BITS, COUNTS>(wa, bits, cnt, first);
-      if (__any_sync(0xFFFFFFFFu, second)) build_unit<L, SMEM_BITS, COUNTS>(wb, bits, cnt, second);
+      build_unit<L, SMEM_BITS, COUNTS>(wa, bits, sbase, cnt, first);
+      if (__any_sync(0xFFFFFFFFu, second)) build_unit<L, SMEM_BITS, COUNTS>(wb, bits, sbase, cnt, second);
     }
     if constexpr (SMEM_BITS) {
       // OR the CTA's non-zero words into the tree's cube bitset.  (Converting
@@ -1001,18 +1018,16 @@ static int launch_build_flat(const uint8_t* frames, int64_t units_per_frame, int
                              uint32_t* ws, uint32_t* out_pyr, int64_t n_trees, uint32_t* zero_cube, int64_t zero_words,
                              uint32_t* counts, cudaStream_t st) {
   constexpr bool SMEM = L <= 6;
-  const size_t smem = SMEM ? size_t(Smem<L>::words) * 4 : 0;
+  const size_t smem = 0;   // the bitset is a static __shared__ array
   // one-time per instantiation: opt in to > 48 KB dynamic smem, cache occupancy
   static int occ[2] = {0, 0};
   int& blocks_per_sm = occ[counts ? 1 : 0];
   if (blocks_per_sm == 0) {
     if (counts) {
       auto k = k_build_flat<L, SMEM, true>;
-      CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       blocks_per_sm = occupancy(k, BUILD_BLOCK, smem);
     } else {
       auto k = k_build_flat<L, SMEM, false>;
-      CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       blocks_per_sm = occupancy(k, BUILD_BLOCK, smem);
     }
   }
