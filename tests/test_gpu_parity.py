@@ -368,3 +368,29 @@ def test_process_batches_pipeline(cuda, golden):
     model, packed = process_batches(train, test, cfg, chunk=16, packed=True)
     cuda.cuda.synchronize()
     assert np.array_equal(packed.numpy(), np.packbits(m.reshape(37, -1).astype(bool), axis=1, bitorder="little"))
+
+
+def test_build_model_abi_and_workspace_contract(cuda):
+    """obg_build_model == build_presence + merge, and the build workspace is
+    handed back all-zero (what lets callers skip clearing it)."""
+    from paper_1412_1945_b200 import _device
+    from paper_1412_1945_b200.model import _WORKSPACES
+    lib = _lib.load()
+    rng = np.random.default_rng(77)
+    for levels, (h, w), grid in [(6, (48, 64), (1, 1)), (5, (33, 20), (2, 3)), (7, (32, 32), (1, 1)),
+                                 (3, (16, 16), (1, 1))]:
+        base = rng.integers(0, 256, size=(1, 1, 1, 3))
+        frames = np.clip(base + rng.integers(-30, 31, size=(10, h, w, 3)), 0, 255).astype(np.uint8)
+        dev = cuda.from_numpy(frames).cuda()
+        cfg = ModelConfig(levels=levels, threshold=0.4, grid_rows=grid[0], grid_cols=grid[1], training_frames=10)
+        model = obg.build_background_model_device(dev, cfg)
+        want = orc.build_background_model(list(frames), levels, 0.4, grid[0], grid[1])
+        for r in range(grid[0]):
+            for c in range(grid[1]):
+                assert model.trees[r][c].to_bytes() == orc.to_bytes(want[(r, c)])
+        pyr = obg.build_presence(dev, levels, grid[0], grid[1])
+        merged, cube = obg.merge_pyramids(pyr, levels, obg.merge_k_min(10, 0.4), with_cube=True)
+        assert cuda.equal(merged, model._dev_pyr) and cuda.equal(cube, model._dev_cube)
+        cuda.cuda.synchronize()
+        for ws in _WORKSPACES.values():
+            assert int(ws.count_nonzero()) == 0
