@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--eager", action="store_true", help="launch kernels eagerly instead of CUDA-graph replay")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=1412)
+    ap.add_argument("--config", type=int, default=3, help="BASELINE.json config index (0..4); 3 is the headline")
+    ap.add_argument("--levels", type=int, default=None, help="octree depth override (config 4 sweeps 4..7)")
+    ap.add_argument("--variant", default="uniform", help="config 4 background: uniform | constant")
     return ap.parse_args()
 
 
@@ -113,13 +116,21 @@ def sha(a) -> str:
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
 
-def golden_record():
+def golden_record(cid, levels, variant):
     try:
         with open(os.path.join(REPO, "tests", "golden", "golden.json")) as f:
             g = json.load(f)
-        return next(r for r in g["configs"] if r["config"] == CONFIG_ID)
+        return next(r for r in g["configs"] if r["config"] == cid and (levels is None or r["levels"] == levels)
+                    and (cid != 4 or r["variant"] == variant))
     except Exception:
         return None
+
+
+def workload_name(scene, n_train, n_test):
+    cfg = scene.config
+    v = f" {scene.variant}" if scene.config_id == 4 else ""
+    return (f"C{scene.config_id}{v} {scene.width}x{scene.height} L{cfg.levels} thr{cfg.threshold}: build model "
+            f"from {n_train} training frames + classify {n_test} test frames per step")
 
 
 # ---------------------------------------------------------------------------
@@ -184,6 +195,8 @@ def cpu_baseline(scene, cfg_kw):
     16 test frames), median of 2, on this box's host."""
     ref = _reference_module()
     train, test = scene.train, scene.test[:16]
+    if scene.config_id == 4:          # 4K stress frames: the reference needs seconds per frame at L=7
+        train, test = scene.train[:4], scene.test[:2]
     times = []
     for _ in range(2):
         t0 = time.perf_counter()
@@ -192,8 +205,9 @@ def cpu_baseline(scene, cfg_kw):
     px = (len(train) + len(test)) * scene.width * scene.height
     return {"value": round(px / statistics.median(times) / 1e6, 3), "unit": "Mpx/s", "cores": 1,
             "kind": "reference" if ref is not None else "port",
-            "sample": f"build_background_model on 64 training + detect_octree on 16 test frames of the "
-                      f"1920x1080 L6 scene, single process, median of 2 ({statistics.median(times):.1f} s)"}
+            "sample": f"build_background_model on {len(train)} training + detect_octree on {len(test)} test frames "
+                      f"of the {scene.width}x{scene.height} L{cfg_kw['levels']} scene, single process, median of 2 "
+                      f"({statistics.median(times):.1f} s)"}
 
 
 def run_reference(args):
@@ -202,8 +216,8 @@ def run_reference(args):
         return
     from multiprocessing import get_context
     from paper_1412_1945_b200 import scenes
-    n_test = 64
-    scene = scenes.generate(CONFIG_ID, seed=args.seed, n_test=n_test)
+    n_test = 64 if args.config != 4 else 4
+    scene = scenes.generate(args.config, seed=args.seed, n_test=n_test, levels=args.levels, variant=args.variant)
     cfg_kw = dict(levels=scene.config.levels, threshold=scene.config.threshold,
                   training_frames=len(scene.train))
     ref = _reference_module()
@@ -228,8 +242,7 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic (seeded scenes with BASELINE config 3 shapes)",
-        "config": {"workload": "C3 1920x1080 L6 thr0.5: build_background_model(64 train) + "
-                               f"detect_octree({n_test} test) per step (bounded sample of the 256-frame batch)",
+        "config": {"workload": workload_name(scene, len(scene.train), n_test) + " (bounded sample of the test batch)",
                    "parallelism": f"fork pool x{cores}" if ref is not None else "1 process (oracle port)"},
         "cpu_baseline": {"value": round(value, 3), "unit": "Mpx/s", "cores": cores if ref is not None else 1,
                          "kind": "reference" if ref is not None else "port",
@@ -268,7 +281,7 @@ def run_ours(args):
     dev = torch.device("cuda", local)
 
     # weak scaling: every rank gets its own seeded scene shard
-    scene = scenes.generate(CONFIG_ID, seed=args.seed + rank)
+    scene = scenes.generate(args.config, seed=args.seed + rank, levels=args.levels, variant=args.variant)
     cfg = scene.config
     P = scene.width * scene.height
     n_train, n_test = len(scene.train), len(scene.test)
@@ -339,7 +352,7 @@ def run_ours(args):
 
     # parity of the timed outputs against the reference's recorded outputs
     parity = None
-    rec = golden_record()
+    rec = golden_record(args.config, args.levels, args.variant)
     if rank == 0 and rec is not None and args.seed == 1412:
         blob = model.trees[0][0].to_bytes()
         m = masks.cpu().numpy()
@@ -414,8 +427,7 @@ def run_ours(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (seeded scenes with BASELINE config 3 shapes: gradient + N(0,3) noise, 20% "
                     "bimodal swaying rows, 10% bootstrapped training frames, 8 moving ellipses)",
-            "config": {"workload": "C3 1920x1080 L6 thr0.5: build model from 64 training frames + classify "
-                                   "256 test frames per step (per rank)",
+            "config": {"workload": workload_name(scene, n_train, n_test) + " (per rank)",
                        "frames_per_step": n_train + n_test, "pixels_per_step": px_step * world,
                        "parallelism": f"dp{world}" + (" (NCCL all-reduce of merge counts)" if world > 1 else ""),
                        "launch": "CUDA graph replay (build graph + classify graph)" if captured else "eager",
