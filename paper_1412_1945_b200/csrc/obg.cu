@@ -158,18 +158,55 @@ __device__ __forceinline__ uint32_t cube_idx(uint32_t x) {
 // Other L: the canonical cube words (idx = R'<<2L | G'<<L | B').
 template <int L>
 struct Smem {
-  static constexpr bool skew = (L == 5 || L == 6);
-  static constexpr uint32_t ROWW = skew ? (1u << (2 * L - 5)) + 1u : 1u;   // words per row incl. pad
+  // every shared-memory level (L <= 6) uses the row layout; L <= 4 rows are
+  // one word per (R', G') holding the 2^L-bit B' row replicated 32/2^L times,
+  // so a funnel shift by any value congruent to B' mod 2^L picks the bit.
+  static constexpr bool skew = (L >= 1 && L <= 6);
+  static constexpr int GW = L > 5 ? (1 << (L - 5)) : 1;                 // words per (R', G')
+  static constexpr uint32_t ROWW = skew ? (uint32_t(GW) << L) + 1u : 1u;  // words per R' row incl. pad
   static constexpr int64_t words = skew ? (int64_t(1) << L) * ROWW : cube_words(L);
-  // canonical cube word -> shared word
+  static constexpr uint32_t REP = L >= 5 ? 1u : L == 4 ? 0x00010001u : L == 3 ? 0x01010101u
+                                  : L == 2 ? 0x11111111u : 0x55555555u;
+  // canonical cube word -> shared word (L >= 5 only: one cube word per shared word)
   __host__ __device__ static constexpr uint32_t phys(uint32_t w) { return skew ? w + (w >> (2 * L - 5)) : w; }
-  // shared word -> canonical cube word, 0xFFFFFFFF for a pad word
+  // shared word -> canonical cube word (L >= 5)
   __device__ static uint32_t canon(uint32_t p) {
     if constexpr (!skew) return p;
     const uint32_t r = p / ROWW, c = p - r * ROWW;
-    return c == ROWW - 1 ? 0xFFFFFFFFu : r * (ROWW - 1) + c;
+    return r * (ROWW - 1) + c;
+  }
+  // bit mask that records B' (= bsel mod 2^L) in a shared word
+  __device__ static uint32_t set_mask(uint32_t bsel) {
+    if constexpr (L >= 5) return 1u << (bsel & 31u);
+    else return REP << (bsel & ((1u << L) - 1u));
   }
 };
+
+// Shared row-layout word p of the classify operand, from the canonical cube.
+template <int L>
+__device__ __forceinline__ uint32_t smem_word_from_cube(const uint32_t* __restrict__ cube, uint32_t p) {
+  const uint32_t r = p / Smem<L>::ROWW, c = p - r * Smem<L>::ROWW;
+  if (c == Smem<L>::ROWW - 1) return 0u;                               // pad
+  if constexpr (L >= 5) {
+    return __ldg(cube + r * (Smem<L>::ROWW - 1) + c);
+  } else {
+    const uint32_t idx = (r << (2 * L)) | (c << L);
+    const uint32_t row = (__ldg(cube + (idx >> 5)) >> (idx & 31u)) & ((1u << L) - 1u);
+    return row * Smem<L>::REP;
+  }
+}
+
+// OR shared row-layout word p (value v) of a build CTA into the tree's canonical cube.
+template <int L>
+__device__ __forceinline__ void flush_smem_word(uint32_t* __restrict__ dst, uint32_t p, uint32_t v) {
+  if constexpr (L >= 5) {
+    atomicOr(dst + Smem<L>::canon(p), v);
+  } else {
+    const uint32_t r = p / Smem<L>::ROWW, c = p - r * Smem<L>::ROWW;
+    const uint32_t idx = (r << (2 * L)) | (c << L);
+    atomicOr(dst + (idx >> 5), (v & ((1u << L) - 1u)) << (idx & 31u));
+  }
+}
 
 // Skewed-layout byte address and bit selector of pixel x = [*, G, B, R].
 // `obase` (optional) is a shared-window base with its low 9 bits clear: it is
@@ -177,10 +214,12 @@ struct Smem {
 template <int L>
 __device__ __forceinline__ void skew_lookup(uint32_t x, uint32_t& addr, uint32_t& bsel, uint32_t obase = 0) {
   constexpr int s = 8 - L;
+  constexpr int gpos = (L > 5 ? L - 5 : 0) + 2;                     // byte-address bit of G' lsb
+  constexpr int gsh = 16 - L - gpos;                                // G' lsb sits at x bit 16-L
   const uint32_t r = __umulhi(x, 1u << (8 - s));                    // x >> (24+s) = R'
-  bsel = __umulhi(x, 1u << (16 - s));                               // x >> (16+s): low 5 bits = B' & 31
-  const uint32_t g = __umulhi(x, 1u << (13 + 2 * L));               // x >> (19-2L): G' at bit L-3
-  uint32_t c = (g & (((1u << L) - 1u) << (L - 3))) | obase;
+  bsel = __umulhi(x, 1u << (16 - s));                               // x >> (16+s): low bits = B'
+  const uint32_t g = __umulhi(x, 1u << (32 - gsh));                 // G' at bit gpos
+  uint32_t c = (g & (((1u << L) - 1u) << gpos)) | obase;
   if constexpr (L == 6) c |= __umulhi(x, 1u << (5 + L)) & 4u;        // x >> (27-L): B'5 at bit 2
   addr = r * (Smem<L>::ROWW * 4u) + c;
 }
@@ -356,7 +395,7 @@ __device__ __forceinline__ void build_unit(const uint32_t (&w)[12], uint32_t* bi
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         if (valid && !(v[j] & 1u)) {
-          if constexpr (SMEM_BITS) reds_or(addr[j], 1u << (bsel[j] & 31u));
+          if constexpr (SMEM_BITS) reds_or(addr[j], Smem<L>::set_mask(bsel[j]));
           else atomicOr(reinterpret_cast<uint32_t*>(base + addr[j]), 1u << (bsel[j] & 31u));
         }
       }
@@ -422,7 +461,7 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
       uint32_t* dst = ws + tree * CW;
       for (int i = threadIdx.x; i < Smem<L>::words; i += BUILD_BLOCK) {
         const uint32_t x = s_bits[i];
-        if (x) { atomicOr(dst + Smem<L>::canon(i), x); s_bits[i] = 0u; }   // pad words stay 0
+        if (x) { flush_smem_word<L>(dst, uint32_t(i), x); s_bits[i] = 0u; }   // pad words stay 0
       }
       __syncthreads();
     }
@@ -830,7 +869,7 @@ k_classify_flat(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_p
   constexpr int64_t CW = cube_words(L);
   const uint32_t* bits = cube;
   if constexpr (SMEM_BITS) {
-    for (int i = threadIdx.x; i < CW; i += CLS_BLOCK) s_bits[Smem<L>::phys(i)] = __ldg(cube + i);
+    for (int i = threadIdx.x; i < Smem<L>::words; i += CLS_BLOCK) s_bits[i] = smem_word_from_cube<L>(cube, i);
     __syncthreads();
     bits = s_bits;
   }
