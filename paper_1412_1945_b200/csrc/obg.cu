@@ -167,6 +167,8 @@ struct Smem {
   static constexpr int64_t words = skew ? (int64_t(1) << L) * ROWW : cube_words(L);
   static constexpr uint32_t REP = L >= 5 ? 1u : L == 4 ? 0x00010001u : L == 3 ? 0x01010101u
                                   : L == 2 ? 0x11111111u : 0x55555555u;
+  // the 2^L-bit B' row of an L <= 4 word
+  static constexpr uint32_t ROWMASK = L >= 5 ? 0xFFFFFFFFu : (1u << (1 << L)) - 1u;
   // canonical cube word -> shared word (L >= 5 only: one cube word per shared word)
   __host__ __device__ static constexpr uint32_t phys(uint32_t w) { return skew ? w + (w >> (2 * L - 5)) : w; }
   // shared word -> canonical cube word (L >= 5)
@@ -191,7 +193,7 @@ __device__ __forceinline__ uint32_t smem_word_from_cube(const uint32_t* __restri
     return __ldg(cube + r * (Smem<L>::ROWW - 1) + c);
   } else {
     const uint32_t idx = (r << (2 * L)) | (c << L);
-    const uint32_t row = (__ldg(cube + (idx >> 5)) >> (idx & 31u)) & ((1u << L) - 1u);
+    const uint32_t row = (__ldg(cube + (idx >> 5)) >> (idx & 31u)) & Smem<L>::ROWMASK;
     return row * Smem<L>::REP;
   }
 }
@@ -204,7 +206,7 @@ __device__ __forceinline__ void flush_smem_word(uint32_t* __restrict__ dst, uint
   } else {
     const uint32_t r = p / Smem<L>::ROWW, c = p - r * Smem<L>::ROWW;
     const uint32_t idx = (r << (2 * L)) | (c << L);
-    atomicOr(dst + (idx >> 5), (v & ((1u << L) - 1u)) << (idx & 31u));
+    atomicOr(dst + (idx >> 5), (v & Smem<L>::ROWMASK) << (idx & 31u));
   }
 }
 
