@@ -830,6 +830,27 @@ constexpr int CLS_BLOCK = 256;
 // Flat path: 1x1 grid, leaf cube bitset in shared memory (L <= 6) or read
 // through L1/L2 (L >= 7).  One thread = one 16-pixel unit per iteration:
 // 3 x 16-byte loads, 16 lookups, one 16-byte (u8) or 2-byte (packed) store.
+// Presence bits (bit 0 of v[j]) of a 16-pixel unit -> 16 foreground mask
+// bytes (one 16-byte streaming store) or 16 mask bits.
+template <bool PACKED>
+__device__ __forceinline__ void store_mask16(const uint32_t (&v)[16], uint8_t* mask, int64_t u) {
+  if constexpr (!PACKED) {
+    uint4 o;
+    o.x = __byte_perm(__byte_perm(v[0], v[1], 0x0040), __byte_perm(v[2], v[3], 0x0040), 0x5410);
+    o.y = __byte_perm(__byte_perm(v[4], v[5], 0x0040), __byte_perm(v[6], v[7], 0x0040), 0x5410);
+    o.z = __byte_perm(__byte_perm(v[8], v[9], 0x0040), __byte_perm(v[10], v[11], 0x0040), 0x5410);
+    o.w = __byte_perm(__byte_perm(v[12], v[13], 0x0040), __byte_perm(v[14], v[15], 0x0040), 0x5410);
+    o.x = ~o.x & 0x01010101u; o.y = ~o.y & 0x01010101u;
+    o.z = ~o.z & 0x01010101u; o.w = ~o.w & 0x01010101u;
+    __stcs(reinterpret_cast<uint4*>(mask) + u, o);
+  } else {
+    uint32_t b = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) b |= (v[j] & 1u) << j;
+    reinterpret_cast<uint16_t*>(mask)[u] = uint16_t(~b & 0xFFFFu);
+  }
+}
+
 // One 16-pixel unit -> 16 mask bytes (or 16 mask bits).
 template <int L, bool SMEM_BITS, bool PACKED>
 __device__ __forceinline__ void classify_unit(const uint32_t (&w)[12], const uint32_t* bits, uint8_t* mask,
@@ -846,21 +867,7 @@ __device__ __forceinline__ void classify_unit(const uint32_t (&w)[12], const uin
     else wd = __ldg(reinterpret_cast<const uint32_t*>(base + addr));
     v[j] = __funnelshift_r(wd, wd, bsel);      // bit 0 = background
   }
-  if constexpr (!PACKED) {
-    uint4 o;
-    o.x = __byte_perm(__byte_perm(v[0], v[1], 0x0040), __byte_perm(v[2], v[3], 0x0040), 0x5410);
-    o.y = __byte_perm(__byte_perm(v[4], v[5], 0x0040), __byte_perm(v[6], v[7], 0x0040), 0x5410);
-    o.z = __byte_perm(__byte_perm(v[8], v[9], 0x0040), __byte_perm(v[10], v[11], 0x0040), 0x5410);
-    o.w = __byte_perm(__byte_perm(v[12], v[13], 0x0040), __byte_perm(v[14], v[15], 0x0040), 0x5410);
-    o.x = ~o.x & 0x01010101u; o.y = ~o.y & 0x01010101u;
-    o.z = ~o.z & 0x01010101u; o.w = ~o.w & 0x01010101u;
-    __stcs(reinterpret_cast<uint4*>(mask) + u, o);
-  } else {
-    uint32_t b = 0;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) b |= (v[j] & 1u) << j;
-    reinterpret_cast<uint16_t*>(mask)[u] = uint16_t(~b & 0xFFFFu);
-  }
+  store_mask16<PACKED>(v, mask, u);
 }
 
 template <int L, bool SMEM_BITS, bool PACKED>
@@ -898,6 +905,91 @@ k_classify_flat(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_p
       }
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// L = 7 classify on a 2-CTA cluster.  The 2^21-bit leaf set (256 KB) does not
+// fit one SM's shared memory, so the pair splits it by R' MSB: each CTA holds
+// 64 R' rows (row = 128 G' x 4 words + 1 skew pad word, 131 KB) and every
+// lookup is an ld.shared::cluster into the owning CTA -- the pixel's R' MSB
+// selects the CTA, nothing else changes.  (The L1/L2 path reached 23 % of
+// HBM on uniform-random frames: every lookup missed L1.)
+// ---------------------------------------------------------------------------
+constexpr int C7_BLOCK = 512;
+constexpr uint32_t C7_ROWW = 513;                          // 512 words + pad
+constexpr uint32_t C7_HALF_WORDS = 64 * C7_ROWW;
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ uint32_t ld_cluster_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+// x = [*, G, B, R] (L = 7, s = 1): R' = x>>25, rank = R'>>6, G' = x[9..15],
+// B' = x[17..23].  Cluster address = base0 + rank*delta + lrow*4*513 + 16 G' + 4 (B'>>5).
+__device__ __forceinline__ uint32_t c7_addr(uint32_t x, uint32_t base0, uint32_t delta) {
+  const uint32_t r = __umulhi(x, 1u << 7);                            // x >> 25
+  const uint32_t rank = __umulhi(x, 2u);                              // x >> 31
+  const uint32_t c = (__umulhi(x, 1u << 27) & (127u << 4)) | (__umulhi(x, 1u << 12) & 0xCu);
+  return rank * delta + (r & 63u) * (C7_ROWW * 4u) + (c | base0);
+}
+
+template <bool PACKED>
+__device__ __forceinline__ void classify_unit_c7(const uint32_t (&w)[12], uint32_t base0, uint32_t delta,
+                                                 uint8_t* mask, int64_t u) {
+  uint32_t px[16], v[16];
+  unpack16<0, 6>(w, px);                                            // [*, G, B, R] operands
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const uint32_t wd = ld_cluster_u32(c7_addr(px[j], base0, delta));
+    v[j] = __funnelshift_r(wd, wd, __umulhi(px[j], 1u << 15));     // x >> 17: B' & 31
+  }
+  store_mask16<PACKED>(v, mask, u);
+}
+
+template <bool PACKED>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C7_BLOCK, 1)
+k_classify_cluster7(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_pixels,
+                    const uint32_t* __restrict__ cube, uint8_t* __restrict__ mask) {
+  extern __shared__ __align__(1024) uint32_t s_half[];
+  const uint32_t rank = cluster_ctarank();
+  for (uint32_t i = threadIdx.x; i < 32768u; i += C7_BLOCK)          // my 64 rows of canonical words
+    s_half[(i >> 9) * C7_ROWW + (i & 511u)] = __ldg(cube + rank * 32768u + i);
+  cluster_sync_all();
+  const uint32_t local = static_cast<uint32_t>(__cvta_generic_to_shared(s_half));
+  const uint32_t base0 = mapa_shared(local, 0), delta = mapa_shared(local, 1) - base0;
+  const int64_t stride = int64_t(gridDim.x) * C7_BLOCK;
+  for (int64_t u = int64_t(blockIdx.x) * C7_BLOCK + threadIdx.x; u < n_units; u += 2 * stride) {
+    const bool second = u + stride < n_units;
+    uint32_t wa[12], wb[12];
+    load_unit(frames, u, wa);
+    if (second) load_unit(frames, u + stride, wb);
+    classify_unit_c7<PACKED>(wa, base0, delta, mask, u);
+    if (second) classify_unit_c7<PACKED>(wb, base0, delta, mask, u + stride);
+  }
+  if constexpr (!PACKED) {
+    if (blockIdx.x == 0) {
+      for (int64_t i = n_units * 16 + threadIdx.x; i < n_pixels; i += C7_BLOCK) {
+        const uint32_t x = gbr_word_scalar(frames + 3 * i);
+        const uint32_t wd = ld_cluster_u32(c7_addr(x, base0, delta));
+        mask[i] = uint8_t(((wd >> ((x >> 17) & 31u)) & 1u) ^ 1u);
+      }
+    }
+  }
+  cluster_sync_all();                                                // peer may still read my half
 }
 
 // Generic path: any grid / alignment / frame size.  One thread = 8 pixels of
@@ -1292,6 +1384,25 @@ static int launch_classify_flat(const uint8_t* frames, int64_t n_pixels, const u
   return OBG_OK;
 }
 
+static int launch_classify_cluster7(const uint8_t* frames, int64_t n_pixels, const uint32_t* cube, uint8_t* mask,
+                                    bool packed, cudaStream_t st) {
+  const size_t smem = size_t(C7_HALF_WORDS) * 4;
+  static bool attr[2] = {false, false};
+  if (!attr[packed]) {
+    if (packed) CUDA_TRY(cudaFuncSetAttribute(k_classify_cluster7<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    else CUDA_TRY(cudaFuncSetAttribute(k_classify_cluster7<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr[packed] = true;
+  }
+  const int64_t n_units = n_pixels / 16;
+  const unsigned grid = unsigned(sm_count() & ~1);        // one CTA per SM, pairs
+  if (packed)
+    k_classify_cluster7<true><<<grid, C7_BLOCK, smem, st>>>(frames, n_units, n_pixels, cube, mask);
+  else
+    k_classify_cluster7<false><<<grid, C7_BLOCK, smem, st>>>(frames, n_units, n_pixels, cube, mask);
+  LAUNCH_CHECK("k_classify_cluster7");
+  return OBG_OK;
+}
+
 int obg_classify(const uint8_t* frames, int n_frames, int height, int width, int levels, int grid_rows, int grid_cols,
                  const uint32_t* cube_bits, uint8_t* mask, int mask_format, void* stream) {
   g_err[0] = 0;
@@ -1318,7 +1429,7 @@ int obg_classify(const uint8_t* frames, int n_frames, int height, int width, int
       case 4: return launch_classify_flat<4>(frames, n_pixels, cube_bits, mask, packed, st);
       case 5: return launch_classify_flat<5>(frames, n_pixels, cube_bits, mask, packed, st);
       case 6: return launch_classify_flat<6>(frames, n_pixels, cube_bits, mask, packed, st);
-      case 7: return launch_classify_flat<7>(frames, n_pixels, cube_bits, mask, packed, st);
+      case 7: return launch_classify_cluster7(frames, n_pixels, cube_bits, mask, packed, st);
       default: return launch_classify_flat<8>(frames, n_pixels, cube_bits, mask, packed, st);
     }
   }
