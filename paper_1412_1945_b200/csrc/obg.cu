@@ -908,88 +908,93 @@ k_classify_flat(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_p
 }
 
 // ---------------------------------------------------------------------------
-// L = 7 classify on a 2-CTA cluster.  The 2^21-bit leaf set (256 KB) does not
-// fit one SM's shared memory, so the pair splits it by R' MSB: each CTA holds
-// 64 R' rows (row = 128 G' x 4 words + 1 skew pad word, 131 KB) and every
-// lookup is an ld.shared::cluster into the owning CTA -- the pixel's R' MSB
-// selects the CTA, nothing else changes.  (The L1/L2 path reached 23 % of
-// HBM on uniform-random frames: every lookup missed L1.)
+// L = 7 classify.  The 2^21-bit leaf set (256 KB) does not fit shared memory,
+// and random lookups through L1 serialise on cache-line tags (ncu/bench r1:
+// 23 % of HBM on uniform-random frames; a 2-CTA cluster splitting the set
+// over DSMEM was slower still).  Instead shared memory holds a 2-bit state
+// per L=6 cell -- no / some / all of its 8 leaves present (64 KB, skewed
+// rows) -- and only pixels in a "some" cell read their leaf bit from the
+// cube in global memory.  Full and empty cells answer from shared memory.
+// State word (R6, G6, B6/16) = SWAR over the 4 cube words of rows
+// (2R6+{0,1}, 2G6+{0,1}): bit pairs (2b, 2b+1) are the children along B'.
 // ---------------------------------------------------------------------------
-constexpr int C7_BLOCK = 512;
-constexpr uint32_t C7_ROWW = 513;                          // 512 words + pad
-constexpr uint32_t C7_HALF_WORDS = 64 * C7_ROWW;
+constexpr int S7_BLOCK = 256;
+constexpr uint32_t S7_ROWW = 257;                          // 64 G6 x 4 words + pad
+constexpr uint32_t S7_WORDS = 64 * S7_ROWW;
 
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ uint32_t ld_cluster_u32(uint32_t addr) {
-  uint32_t v;
-  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr));
-  return v;
+__device__ __forceinline__ uint32_t s7_state_word(const uint32_t* __restrict__ cube, uint32_t i) {
+  const uint32_t r6 = i >> 8, g6 = (i >> 2) & 63u, q = i & 3u;
+  const uint32_t b = (2u * r6) * 512u + (2u * g6) * 4u + q;
+  const uint32_t w00 = __ldg(cube + b), w01 = __ldg(cube + b + 4), w10 = __ldg(cube + b + 512);
+  const uint32_t w11 = __ldg(cube + b + 516);
+  const uint32_t a = w00 | w01 | w10 | w11, A = w00 & w01 & w10 & w11;
+  return ((a | (a >> 1)) & 0x55555555u) | (((A & (A >> 1)) & 0x55555555u) << 1);
 }
 
-// x = [*, G, B, R] (L = 7, s = 1): R' = x>>25, rank = R'>>6, G' = x[9..15],
-// B' = x[17..23].  Cluster address = base0 + rank*delta + lrow*4*513 + 16 G' + 4 (B'>>5).
-__device__ __forceinline__ uint32_t c7_addr(uint32_t x, uint32_t base0, uint32_t delta) {
-  const uint32_t r = __umulhi(x, 1u << 7);                            // x >> 25
-  const uint32_t rank = __umulhi(x, 2u);                              // x >> 31
-  const uint32_t c = (__umulhi(x, 1u << 27) & (127u << 4)) | (__umulhi(x, 1u << 12) & 0xCu);
-  return rank * delta + (r & 63u) * (C7_ROWW * 4u) + (c | base0);
+// x = [*, G, B, R] (s = 1): R6 = x>>26, G6 = x[10..15], B6 = x[18..23].
+// Returns the cell's state in bits 0 (some) and 1 (all).
+__device__ __forceinline__ uint32_t s7_state(const uint32_t* s_state, uint32_t x) {
+  const uint32_t r6 = __umulhi(x, 1u << 6);                          // x >> 26
+  const uint32_t c = (__umulhi(x, 1u << 26) & (63u << 4)) | (__umulhi(x, 1u << 12) & 0xCu);
+  const uint32_t w = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(s_state) +
+                                                          r6 * (S7_ROWW * 4u) + c);
+  return __funnelshift_r(w, w, __umulhi(x, 1u << 15) & 0x1Eu);       // (B6 & 15) * 2
+}
+
+__device__ __forceinline__ uint32_t l7_leaf_bit(const uint32_t* __restrict__ cube, uint32_t x) {
+  const uint32_t idx = ((x >> 25) << 14) | (((x >> 9) & 127u) << 7) | ((x >> 17) & 127u);
+  return (__ldg(cube + (idx >> 5)) >> (idx & 31u)) & 1u;
 }
 
 template <bool PACKED>
-__device__ __forceinline__ void classify_unit_c7(const uint32_t (&w)[12], uint32_t base0, uint32_t delta,
-                                                 uint8_t* mask, int64_t u) {
+__device__ __forceinline__ void classify_unit_l7(const uint32_t (&w)[12], const uint32_t* s_state,
+                                                 const uint32_t* __restrict__ cube, uint8_t* mask, int64_t u) {
   uint32_t px[16], v[16];
   unpack16<0, 6>(w, px);                                            // [*, G, B, R] operands
+  uint32_t mixed = 0;
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
-    const uint32_t wd = ld_cluster_u32(c7_addr(px[j], base0, delta));
-    v[j] = __funnelshift_r(wd, wd, __umulhi(px[j], 1u << 15));     // x >> 17: B' & 31
+    const uint32_t st = s7_state(s_state, px[j]);
+    v[j] = st >> 1;                                                 // all children present
+    mixed |= (st ^ (st >> 1)) & 1u;                                 // some but not all
+  }
+  if (__any_sync(__activemask(), mixed)) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t st = s7_state(s_state, px[j]);
+      if ((st ^ (st >> 1)) & 1u) v[j] = l7_leaf_bit(cube, px[j]);
+    }
   }
   store_mask16<PACKED>(v, mask, u);
 }
 
 template <bool PACKED>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C7_BLOCK, 1)
-k_classify_cluster7(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_pixels,
-                    const uint32_t* __restrict__ cube, uint8_t* __restrict__ mask) {
-  extern __shared__ __align__(1024) uint32_t s_half[];
-  const uint32_t rank = cluster_ctarank();
-  for (uint32_t i = threadIdx.x; i < 32768u; i += C7_BLOCK)          // my 64 rows of canonical words
-    s_half[(i >> 9) * C7_ROWW + (i & 511u)] = __ldg(cube + rank * 32768u + i);
-  cluster_sync_all();
-  const uint32_t local = static_cast<uint32_t>(__cvta_generic_to_shared(s_half));
-  const uint32_t base0 = mapa_shared(local, 0), delta = mapa_shared(local, 1) - base0;
-  const int64_t stride = int64_t(gridDim.x) * C7_BLOCK;
-  for (int64_t u = int64_t(blockIdx.x) * C7_BLOCK + threadIdx.x; u < n_units; u += 2 * stride) {
+__global__ void __launch_bounds__(S7_BLOCK, 2)
+k_classify_l7(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_pixels, const uint32_t* __restrict__ cube,
+              uint8_t* __restrict__ mask) {
+  extern __shared__ uint32_t s_state[];
+  for (uint32_t i = threadIdx.x; i < 64u * 256u; i += S7_BLOCK) s_state[(i >> 8) * S7_ROWW + (i & 255u)] =
+      s7_state_word(cube, i);
+  __syncthreads();
+  const int64_t stride = int64_t(gridDim.x) * S7_BLOCK;
+  for (int64_t u = int64_t(blockIdx.x) * S7_BLOCK + threadIdx.x; u < n_units; u += 2 * stride) {
     const bool second = u + stride < n_units;
     uint32_t wa[12], wb[12];
     load_unit(frames, u, wa);
     if (second) load_unit(frames, u + stride, wb);
-    classify_unit_c7<PACKED>(wa, base0, delta, mask, u);
-    if (second) classify_unit_c7<PACKED>(wb, base0, delta, mask, u + stride);
+    classify_unit_l7<PACKED>(wa, s_state, cube, mask, u);
+    if (second) classify_unit_l7<PACKED>(wb, s_state, cube, mask, u + stride);
   }
   if constexpr (!PACKED) {
     if (blockIdx.x == 0) {
-      for (int64_t i = n_units * 16 + threadIdx.x; i < n_pixels; i += C7_BLOCK) {
+      for (int64_t i = n_units * 16 + threadIdx.x; i < n_pixels; i += S7_BLOCK) {
         const uint32_t x = gbr_word_scalar(frames + 3 * i);
-        const uint32_t wd = ld_cluster_u32(c7_addr(x, base0, delta));
-        mask[i] = uint8_t(((wd >> ((x >> 17) & 31u)) & 1u) ^ 1u);
+        const uint32_t st = s7_state(s_state, x);
+        const uint32_t bg = ((st ^ (st >> 1)) & 1u) ? l7_leaf_bit(cube, x) : (st >> 1) & 1u;
+        mask[i] = uint8_t(bg ^ 1u);
       }
     }
   }
-  cluster_sync_all();                                                // peer may still read my half
 }
 
 // Generic path: any grid / alignment / frame size.  One thread = 8 pixels of
@@ -1384,22 +1389,30 @@ static int launch_classify_flat(const uint8_t* frames, int64_t n_pixels, const u
   return OBG_OK;
 }
 
-static int launch_classify_cluster7(const uint8_t* frames, int64_t n_pixels, const uint32_t* cube, uint8_t* mask,
-                                    bool packed, cudaStream_t st) {
-  const size_t smem = size_t(C7_HALF_WORDS) * 4;
-  static bool attr[2] = {false, false};
-  if (!attr[packed]) {
-    if (packed) CUDA_TRY(cudaFuncSetAttribute(k_classify_cluster7<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    else CUDA_TRY(cudaFuncSetAttribute(k_classify_cluster7<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr[packed] = true;
+static int launch_classify_l7(const uint8_t* frames, int64_t n_pixels, const uint32_t* cube, uint8_t* mask,
+                              bool packed, cudaStream_t st) {
+  const size_t smem = size_t(S7_WORDS) * 4;
+  static int occ[2] = {0, 0};
+  int& bps = occ[packed ? 1 : 0];
+  if (bps == 0) {
+    if (packed) {
+      CUDA_TRY(cudaFuncSetAttribute(k_classify_l7<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      bps = occupancy(k_classify_l7<true>, S7_BLOCK, smem);
+    } else {
+      CUDA_TRY(cudaFuncSetAttribute(k_classify_l7<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      bps = occupancy(k_classify_l7<false>, S7_BLOCK, smem);
+    }
   }
   const int64_t n_units = n_pixels / 16;
-  const unsigned grid = unsigned(sm_count() & ~1);        // one CTA per SM, pairs
+  int64_t grid = int64_t(sm_count()) * bps;
+  const int64_t need = (n_units + S7_BLOCK - 1) / S7_BLOCK;
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
   if (packed)
-    k_classify_cluster7<true><<<grid, C7_BLOCK, smem, st>>>(frames, n_units, n_pixels, cube, mask);
+    k_classify_l7<true><<<unsigned(grid), S7_BLOCK, smem, st>>>(frames, n_units, n_pixels, cube, mask);
   else
-    k_classify_cluster7<false><<<grid, C7_BLOCK, smem, st>>>(frames, n_units, n_pixels, cube, mask);
-  LAUNCH_CHECK("k_classify_cluster7");
+    k_classify_l7<false><<<unsigned(grid), S7_BLOCK, smem, st>>>(frames, n_units, n_pixels, cube, mask);
+  LAUNCH_CHECK("k_classify_l7");
   return OBG_OK;
 }
 
@@ -1429,7 +1442,7 @@ int obg_classify(const uint8_t* frames, int n_frames, int height, int width, int
       case 4: return launch_classify_flat<4>(frames, n_pixels, cube_bits, mask, packed, st);
       case 5: return launch_classify_flat<5>(frames, n_pixels, cube_bits, mask, packed, st);
       case 6: return launch_classify_flat<6>(frames, n_pixels, cube_bits, mask, packed, st);
-      case 7: return launch_classify_cluster7(frames, n_pixels, cube_bits, mask, packed, st);
+      case 7: return launch_classify_l7(frames, n_pixels, cube_bits, mask, packed, st);
       default: return launch_classify_flat<8>(frames, n_pixels, cube_bits, mask, packed, st);
     }
   }
