@@ -21,8 +21,10 @@
  *            path code (octree.py:70-80, l octal digits) is c exists.  Level-l
  *            word count = max(1, 8^l / 32).  The child mask byte of node p at
  *            level l (octree.py:217-227) is byte p of level l+1.
- *   cube     u32 [obg_cube_words(L)]           kernel-internal leaf bitset in
- *            "RGB cube" order: idx = R'<<2L | G'<<L | B' with C' = C >> (8-L).
+ *   cube     u32 [obg_cube_words(L)]           classify operand: leaf bitset in
+ *            "RGB cube" order, idx = R'<<2L | G'<<L | B' with C' = C >> (8-L)
+ *            (max(1, 8^L/32) words); for L = 7 followed by a 2-bit state per
+ *            L=6 cell (16384 words: some / all of its 8 leaves present).
  *   mask     u8  [n_frames][height][width]     0/1 (numpy bool layout), or
  *            bit-packed u8 [n_frames][ceil(h*w/8)], LSB-first per frame.
  */

@@ -110,4 +110,6 @@ def level_offset(level: int) -> int:
 
 
 def cube_words(levels: int) -> int:
-    return level_words(levels)
+    """Words of one region's classify operand: the leaf cube, plus for L = 7
+    a 2-bit state per L=6 cell (16384 words)."""
+    return level_words(levels) + (16384 if levels == 7 else 0)

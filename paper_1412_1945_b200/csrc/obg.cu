@@ -69,6 +69,12 @@ __host__ __device__ static constexpr int64_t level_offset(int l) {
 }
 __host__ __device__ static constexpr int64_t pyr_words(int L) { return level_offset(L + 1); }
 __host__ __device__ static constexpr int64_t cube_words(int L) { return level_words(L); }
+// Classify operand per region: the leaf cube, plus for L = 7 a 2-bit state
+// per L=6 cell (16384 words, see k_classify_l7).
+constexpr int64_t S7_CANON_WORDS = 16384;
+__host__ __device__ static constexpr int64_t operand_words(int L) {
+  return cube_words(L) + (L == 7 ? S7_CANON_WORDS : 0);
+}
 
 constexpr int PYR_CHUNK = 1024;  // k_pyramid: leaf-level words per CTA (a 32x32x32 sub-cube)
 
@@ -676,7 +682,7 @@ __device__ __forceinline__ void finish_word(const uint32_t (&c32)[32], int64_t w
 #pragma unroll
     for (int b = 0; b < 32; ++b) bits |= uint32_t(int64_t(c32[b]) >= k_min) << b;
     out[wi] = bits;
-    if (cube && w >= leaf_off) scatter_leaf_word_to_cube(bits, uint32_t(w - leaf_off), L, cube + r * CW);
+    if (cube && w >= leaf_off) scatter_leaf_word_to_cube(bits, uint32_t(w - leaf_off), L, cube + r * operand_words(L));
   }
 }
 
@@ -766,7 +772,7 @@ k_merge(const uint32_t* __restrict__ pyr, int n_trees, int n_regions, int L, int
       for (int g = 0; g < MERGE_GROUPS; ++g) bits |= s_bits[g][x];
       out[wi] = bits;
       const int64_t r = wi / PW, w = wi - r * PW;
-      if (cube && w >= leaf_off) scatter_leaf_word_to_cube(bits, uint32_t(w - leaf_off), L, cube + r * CW);
+      if (cube && w >= leaf_off) scatter_leaf_word_to_cube(bits, uint32_t(w - leaf_off), L, cube + r * operand_words(L));
     }
     __syncthreads();
   }
@@ -809,7 +815,7 @@ __global__ void k_leaf_cube(const uint32_t* __restrict__ pyr, int64_t PW, int L,
   const int64_t CW = cube_words(L);
   const int64_t off = level_offset(L);
   const int64_t total = CW * n_trees;
-  const int nbits = L == 1 ? 8 : 32;
+  const int nbits = L == 1 ? 8 : 32;   // writes the cube part of each region's operand
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t t = i / CW, cw = i - t * CW;
     const uint32_t* leaf = pyr + t * PW + off;
@@ -818,7 +824,25 @@ __global__ void k_leaf_cube(const uint32_t* __restrict__ pyr, int64_t PW, int L,
       const uint32_t code = cube_to_code(uint32_t(cw * 32 + b), L);
       v |= ((__ldg(leaf + (code >> 5)) >> (code & 31u)) & 1u) << b;
     }
-    cube[i] = v;
+    cube[t * operand_words(L) + cw] = v;
+  }
+}
+
+// L = 7 classify operand: 2-bit state per L=6 cell from the finished cube
+// (some / all of its 8 leaves present), canonical order i = R6*256 + G6*4 + B6/16,
+// stored after the cube.  State word = SWAR over the 4 cube words of rows
+// (2R6+{0,1}, 2G6+{0,1}): bit pairs (2b, 2b+1) are the children along B'.
+__global__ void k_l7_states(uint32_t* __restrict__ operand, int64_t n_regions) {
+  const int64_t total = S7_CANON_WORDS * n_regions;
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < total; k += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = k / S7_CANON_WORDS;
+    const uint32_t i = uint32_t(k - r * S7_CANON_WORDS);
+    uint32_t* op = operand + r * operand_words(7);
+    const uint32_t r6 = i >> 8, g6 = (i >> 2) & 63u, q = i & 3u;
+    const uint32_t b = (2u * r6) * 512u + (2u * g6) * 4u + q;
+    const uint32_t w00 = op[b], w01 = op[b + 4], w10 = op[b + 512], w11 = op[b + 516];
+    const uint32_t a = w00 | w01 | w10 | w11, A = w00 & w01 & w10 & w11;
+    op[cube_words(7) + i] = ((a | (a >> 1)) & 0x55555555u) | (((A & (A >> 1)) & 0x55555555u) << 1);
   }
 }
 
@@ -922,15 +946,6 @@ constexpr int S7_BLOCK = 256;
 constexpr uint32_t S7_ROWW = 257;                          // 64 G6 x 4 words + pad
 constexpr uint32_t S7_WORDS = 64 * S7_ROWW;
 
-__device__ __forceinline__ uint32_t s7_state_word(const uint32_t* __restrict__ cube, uint32_t i) {
-  const uint32_t r6 = i >> 8, g6 = (i >> 2) & 63u, q = i & 3u;
-  const uint32_t b = (2u * r6) * 512u + (2u * g6) * 4u + q;
-  const uint32_t w00 = __ldg(cube + b), w01 = __ldg(cube + b + 4), w10 = __ldg(cube + b + 512);
-  const uint32_t w11 = __ldg(cube + b + 516);
-  const uint32_t a = w00 | w01 | w10 | w11, A = w00 & w01 & w10 & w11;
-  return ((a | (a >> 1)) & 0x55555555u) | (((A & (A >> 1)) & 0x55555555u) << 1);
-}
-
 // x = [*, G, B, R] (s = 1): R6 = x>>26, G6 = x[10..15], B6 = x[18..23].
 // Returns the cell's state in bits 0 (some) and 1 (all).
 __device__ __forceinline__ uint32_t s7_state(const uint32_t* s_state, uint32_t x) {
@@ -954,27 +969,31 @@ __device__ __forceinline__ void classify_unit_l7(const uint32_t (&w)[12], const 
   uint32_t mixed = 0;
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
-    const uint32_t st = s7_state(s_state, px[j]);
-    v[j] = st >> 1;                                                 // all children present
-    mixed |= (st ^ (st >> 1)) & 1u;                                 // some but not all
+    v[j] = s7_state(s_state, px[j]);
+    mixed |= (v[j] ^ (v[j] >> 1)) & 1u;                             // some but not all leaves
   }
   if (__any_sync(__activemask(), mixed)) {
+    // branch-free: every pixel of the unit reads its leaf bit (L1-resident
+    // when the cells are few), partial cells take it
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const uint32_t st = s7_state(s_state, px[j]);
-      if ((st ^ (st >> 1)) & 1u) v[j] = l7_leaf_bit(cube, px[j]);
+      const uint32_t leaf = l7_leaf_bit(cube, px[j]);
+      v[j] = ((v[j] ^ (v[j] >> 1)) & 1u) ? leaf : (v[j] >> 1);
     }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] >>= 1;                        // all children present
   }
   store_mask16<PACKED>(v, mask, u);
 }
 
 template <bool PACKED>
-__global__ void __launch_bounds__(S7_BLOCK, 2)
+__global__ void __launch_bounds__(S7_BLOCK, 3)
 k_classify_l7(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_pixels, const uint32_t* __restrict__ cube,
               uint8_t* __restrict__ mask) {
   extern __shared__ uint32_t s_state[];
-  for (uint32_t i = threadIdx.x; i < 64u * 256u; i += S7_BLOCK) s_state[(i >> 8) * S7_ROWW + (i & 255u)] =
-      s7_state_word(cube, i);
+  for (uint32_t i = threadIdx.x; i < 64u * 256u; i += S7_BLOCK)       // states follow the cube (k_l7_states)
+    s_state[(i >> 8) * S7_ROWW + (i & 255u)] = __ldg(cube + cube_words(7) + i);
   __syncthreads();
   const int64_t stride = int64_t(gridDim.x) * S7_BLOCK;
   for (int64_t u = int64_t(blockIdx.x) * S7_BLOCK + threadIdx.x; u < n_units; u += 2 * stride) {
@@ -1020,7 +1039,7 @@ k_classify_generic(const uint8_t* __restrict__ frames, int64_t n_frames, int H, 
       const uint8_t* px = frames + 3 * (f * P + p);
       const uint32_t idx = ((uint32_t(px[0]) >> s) << (2 * L)) | ((uint32_t(px[1]) >> s) << L) |
                            (uint32_t(px[2]) >> s);
-      const uint32_t* bits = cube + (int64_t(row) * C + col) * CW;
+      const uint32_t* bits = cube + (int64_t(row) * C + col) * operand_words(L);
       const uint32_t fg = ((__ldg(bits + (idx >> 5)) >> (idx & 31u)) & 1u) ^ 1u;
       if (PACKED) byte |= fg << k;
       else mask[f * P + p] = uint8_t(fg);
@@ -1134,7 +1153,7 @@ int64_t obg_level_offset(int levels, int level) {
   if (levels < 1 || levels > 8 || level < 1 || level > levels) return -1;
   return level_offset(level);
 }
-int64_t obg_cube_words(int levels) { return (levels < 1 || levels > 8) ? -1 : cube_words(levels); }
+int64_t obg_cube_words(int levels) { return (levels < 1 || levels > 8) ? -1 : operand_words(levels); }
 int64_t obg_build_workspace_bytes(int n_trees, int n_regions, int levels) {
   if (levels < 1 || levels > 8 || n_trees < 0 || n_regions < 1) return -1;
   return int64_t(n_trees) * n_regions * cube_words(levels) * 4;
@@ -1276,7 +1295,7 @@ int obg_build_model(const uint8_t* frames, int n_frames, int height, int width, 
   // the build kernel clears the cube the merge scatters into: no memsets at all
   int rc = build_presence_impl(frames, n_frames, height, width, levels, grid_rows, grid_cols, group_size,
                                tree_pyramids, nullptr, workspace, workspace_bytes, flags, out_cube,
-                               n_regions * cube_words(levels), stream);
+                               n_regions * operand_words(levels), stream);
   if (rc != OBG_OK) return rc;
   return merge_common(tree_pyramids, n_frames / group_size, int(n_regions), levels, k_min, nullptr, out_merged,
                       out_cube, OBG_CUBE_ZEROED, stream);
@@ -1308,6 +1327,13 @@ int obg_prune(const uint32_t* pyramids, int n_trees, int levels, int new_levels,
   return OBG_OK;
 }
 
+static int finish_operand(uint32_t* operand, int64_t n_regions, int levels, cudaStream_t st) {
+  if (levels != 7 || !operand) return OBG_OK;
+  k_l7_states<<<grid_for(S7_CANON_WORDS * n_regions, 256, sm_count() * 8), 256, 0, st>>>(operand, n_regions);
+  LAUNCH_CHECK("k_l7_states");
+  return OBG_OK;
+}
+
 static int merge_common(const uint32_t* pyramids, int n_trees, int n_regions, int levels, int64_t k_min,
                         uint32_t* counts, uint32_t* out, uint32_t* out_cube, int flags, void* stream) {
   if (levels < 1 || levels > 8) return set_err(OBG_EINVAL, "levels must be in 1..8, got %d", levels);
@@ -1316,12 +1342,12 @@ static int merge_common(const uint32_t* pyramids, int n_trees, int n_regions, in
   if (!pyramids) return set_err(OBG_EINVAL, "null buffer");
   cudaStream_t st = as_stream(stream);
   if (out_cube && !(flags & OBG_CUBE_ZEROED))
-    CUDA_TRY(cudaMemsetAsync(out_cube, 0, size_t(n_regions) * cube_words(levels) * 4, st));
+    CUDA_TRY(cudaMemsetAsync(out_cube, 0, size_t(n_regions) * operand_words(levels) * 4, st));
   const int64_t words = pyr_words(levels) * n_regions;
   k_merge<<<grid_for(words, 32, sm_count() * 16), dim3(32, MERGE_GROUPS), 0, st>>>(
       pyramids, n_trees, n_regions, levels, k_min, counts, out, out_cube);
   LAUNCH_CHECK("k_merge");
-  return OBG_OK;
+  return finish_operand(out_cube, n_regions, levels, st);
 }
 
 int obg_merge_counts(const uint32_t* pyramids, int n_trees, int n_regions, int levels, uint32_t* counts, void* stream) {
@@ -1346,12 +1372,12 @@ int obg_merge_threshold(const uint32_t* counts, int n_regions, int levels, int64
   if (k_min < 1) return set_err(OBG_EINVAL, "k_min must be >= 1, got %lld", (long long)k_min);
   if (!counts || !out_pyramids) return set_err(OBG_EINVAL, "null buffer");
   cudaStream_t st = as_stream(stream);
-  if (out_cube) CUDA_TRY(cudaMemsetAsync(out_cube, 0, size_t(n_regions) * cube_words(levels) * 4, st));
+  if (out_cube) CUDA_TRY(cudaMemsetAsync(out_cube, 0, size_t(n_regions) * operand_words(levels) * 4, st));
   const int64_t words = pyr_words(levels) * n_regions;
   k_threshold<<<grid_for(words, 256, sm_count() * 8), 256, 0, st>>>(counts, n_regions, levels, k_min,
                                                                    out_pyramids, out_cube);
   LAUNCH_CHECK("k_threshold");
-  return OBG_OK;
+  return finish_operand(out_cube, n_regions, levels, st);
 }
 
 int obg_leaf_cube(const uint32_t* pyramids, int n_trees, int levels, uint32_t* cube, void* stream) {
@@ -1364,7 +1390,7 @@ int obg_leaf_cube(const uint32_t* pyramids, int n_trees, int levels, uint32_t* c
   k_leaf_cube<<<grid_for(CW * n_trees, 256, sm_count() * 8), 256, 0, as_stream(stream)>>>(
       pyramids, pyr_words(levels), levels, n_trees, cube);
   LAUNCH_CHECK("k_leaf_cube");
-  return OBG_OK;
+  return finish_operand(cube, n_trees, levels, as_stream(stream));
 }
 
 template <int L>
