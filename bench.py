@@ -378,7 +378,7 @@ def run_ours(args):
                 out = obg.classify(model, h_test.to(dev, non_blocking=True), out=masks)
                 h_masks.copy_(out, non_blocking=True)
             else:
-                process_batches(h_train, h_test, cfg, out_host=h_masks, chunk=32)
+                process_batches(h_train, h_test, cfg, out_host=h_masks, chunk=8)
 
         for _ in range(2):
             e2e_step()
@@ -400,7 +400,7 @@ def run_ours(args):
                "h2d_bytes_per_step": int(h_train.numel() + h_test.numel()),
                "d2h_bytes_per_step": int(h_masks.numel()), "ms_per_step": round(e_ms, 3),
                "path": "pipeline.process_batches: pinned host frames -> H2D (copy stream) -> build + classify "
-                       "in 32-frame chunks -> mask D2H (second copy stream), copies overlapped with kernels"
+                       "in 8-frame chunks -> mask D2H (second copy stream), copies overlapped with kernels"
                        if world == 1 else "eager H2D + sharded build + classify + D2H"}
 
     peak, peak_src = peaks()
