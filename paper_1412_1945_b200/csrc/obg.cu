@@ -937,17 +937,29 @@ __device__ __forceinline__ void store_mask16(const uint32_t (&v)[16], uint8_t* m
 template <int L, bool SMEM_BITS, bool PACKED>
 __device__ __forceinline__ void classify_unit(const uint32_t (&w)[12], const uint32_t* bits, uint8_t* mask,
                                               int64_t u) {
-  uint32_t px[16];
-  unpack16<0, L>(w, px);
   const char* base = reinterpret_cast<const char*>(bits);
   uint32_t v[16];
+  if constexpr (SMEM_BITS) {
+    // two pixels per address computation (see pair_positions)
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    uint32_t addr, bsel, wd;
-    bit_position<L>(px[j], addr, bsel);
-    if constexpr (SMEM_BITS) wd = *reinterpret_cast<const uint32_t*>(base + addr);
-    else wd = __ldg(reinterpret_cast<const uint32_t*>(base + addr));
-    v[j] = __funnelshift_r(wd, wd, bsel);      // bit 0 = background
+    for (int k = 0; k < 8; ++k) {
+      uint32_t aa, ba, ab, bb;
+      pair_positions_dyn<L>(w, k, 0u, aa, ba, ab, bb);
+      const uint32_t wa = *reinterpret_cast<const uint32_t*>(base + aa);
+      const uint32_t wb = *reinterpret_cast<const uint32_t*>(base + ab);
+      v[2 * k] = __funnelshift_r(wa, wa, ba);                       // bit 0 = background
+      v[2 * k + 1] = __funnelshift_r(wb, wb, bb);
+    }
+  } else {
+    uint32_t px[16];
+    unpack16<0, L>(w, px);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      uint32_t addr, bsel;
+      bit_position<L>(px[j], addr, bsel);
+      const uint32_t wd = __ldg(reinterpret_cast<const uint32_t*>(base + addr));
+      v[j] = __funnelshift_r(wd, wd, bsel);
+    }
   }
   store_mask16<PACKED>(v, mask, u);
 }
