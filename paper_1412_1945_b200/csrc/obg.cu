@@ -152,36 +152,71 @@ __device__ __forceinline__ uint32_t cube_idx(uint32_t x) {
 
 // Shared-memory layout of the leaf bitset used by the streaming kernels.
 //
-// L = 5, 6 ("skewed rows"): row R' holds the 2^(2L-5) words (G', B'>>5) of
-// the cube plus one pad word, so consecutive R' rows start one bank apart.
-// Without the skew every R' value of a warp lands in the same bank and a
-// warp reading a colour gradient serialises (ncu r1: 6.6x the ideal shared
-// wavefronts).  A pixel's byte address and bit are computed from
-// x = [*, G, B, R] with multiply-high shifts (FMA pipe) so that the ALU pipe,
-// which bounds these kernels (ncu r3: 85 % busy), only sees the masks:
-//   A   = R' * 4*ROWW + G' << (L-3) | (B' >> 5) << 2
-//   bit = B' & 31
+// Row layout ("skewed rows", every L <= 6): row R' holds the words of
+// (R', G', *) plus PAD pad words, so consecutive R' rows start PAD banks
+// apart.  Without the skew every R' value of a warp lands in the same bank
+// and a warp reading a colour gradient serialises (ncu r1: 6.6x the ideal
+// shared wavefronts).  A pixel's byte address and bit are computed from
+// x = [*, G, B, R] with multiply-high shifts (FMA pipe) and masks (ALU).
+//
+// L = 6, build kernel (SPLIT): two halves by B'5 = B' >> 5, 32 KB apart: word
+// B'5 * 8192 + R' * ROWW + G', bit B' & 31.  The in-row byte offset of a pixel
+// is then G & 0xFC | (B & 0x80) << 8 -- ONE mask of the 16-bit value
+// G | B << 8, which the pair addressing (pair_positions) gets for free from its
+// byte permute.  Words 64*ROWW .. 8191 are a hole (the build kernel keeps its
+// per-lane dummy words there).  The classify kernel keeps the compact L = 6
+// layout -- row R' = 64 x (G', B'5) words + pad, 36 KB -- because the 53 KB
+// split span at 4 CTAs/SM leaves L1 too small for the 48-byte unit loads,
+// whose three 16-byte pieces per lane share 128-byte lines (bench r10:
+// classify 0.317 -> 0.399 ms with the split layout).
+// L = 5: word R' * ROWW + G' (one 32-bit B' row per word).
+// L <= 4: one word per (R', G') holding the 2^L-bit B' row replicated
+// 32/2^L times, so a funnel shift by any value congruent to B' mod 2^L picks
+// the bit.
 // Other L: the canonical cube words (idx = R'<<2L | G'<<L | B').
-template <int L>
-struct Smem {
-  // every shared-memory level (L <= 6) uses the row layout; L <= 4 rows are
-  // one word per (R', G') holding the 2^L-bit B' row replicated 32/2^L times,
-  // so a funnel shift by any value congruent to B' mod 2^L picks the bit.
+template <int L_, bool SPLIT>
+struct SmemT {
+  static constexpr int L = L_;
   static constexpr bool skew = (L >= 1 && L <= 6);
-  static constexpr int GW = L > 5 ? (1 << (L - 5)) : 1;                 // words per (R', G')
-  static constexpr uint32_t ROWW = skew ? (uint32_t(GW) << L) + 1u : 1u;  // words per R' row incl. pad
-  static constexpr int64_t words = skew ? (int64_t(1) << L) * ROWW : cube_words(L);
+  static constexpr bool split = SPLIT && L == 6;
+  static constexpr uint32_t GW = (L == 6 && !split) ? 2u : 1u;       // words per (R', G')
+  // pad words per R' row: the row stride mod 32 sets the bank step between
+  // neighbouring R' values; these minimise the max distinct words per bank
+  // for a warp's 32 lookups on the C1-C3 scenes (tools/banksim.py: L6
+  // 3.04 -> 2.16 wavefronts per lookup, L5 2.31 -> 1.31, L4 1.06 -> 1.00)
+  static constexpr uint32_t PAD = L == 6 ? (split ? 14u : 13u) : L == 5 ? 14u : L == 4 ? 2u : 1u;
+  static constexpr uint32_t ROWW = skew ? (GW << L) + PAD : 1u;        // words per R' row incl. pad
+  static constexpr uint32_t ROWS = skew ? (1u << L) * ROWW : 0u;       // words of the rows (one half if split)
+  static constexpr uint32_t HALF = 8192u;                              // split: word offset of B'5 = 1
+  // words spanned (hole included), and the words holding data ("compact"
+  // index i -> word compact_word(i))
+  static constexpr int64_t words = split ? HALF + ROWS : skew ? ROWS : cube_words(L);
+  static constexpr uint32_t compact = split ? 2u * ROWS : uint32_t(words);
+  // first of 32 per-lane dummy words (build kernel atomics that must not land)
+  static constexpr uint32_t DUMMY = split ? ROWS : uint32_t(words);
+  static constexpr int64_t alloc_words = split ? words : words + 32;
+  static_assert(!split || ROWS + 32 <= HALF, "split halves overlap");
   static constexpr uint32_t REP = L >= 5 ? 1u : L == 4 ? 0x00010001u : L == 3 ? 0x01010101u
                                   : L == 2 ? 0x11111111u : 0x55555555u;
   // the 2^L-bit B' row of an L <= 4 word
   static constexpr uint32_t ROWMASK = L >= 5 ? 0xFFFFFFFFu : (1u << (1 << L)) - 1u;
-  // canonical cube word -> shared word (L >= 5 only: one cube word per shared word)
-  __host__ __device__ static constexpr uint32_t phys(uint32_t w) { return skew ? w + (w >> (2 * L - 5)) : w; }
-  // shared word -> canonical cube word (L >= 5)
+  __host__ __device__ static constexpr uint32_t compact_word(uint32_t i) {
+    return split && i >= ROWS ? i - ROWS + HALF : i;
+  }
+  // shared word p -> (half, R', column); column >= GW * 2^L is a pad word
+  __device__ static void locate(uint32_t p, uint32_t& h, uint32_t& r, uint32_t& c) {
+    h = split && p >= HALF ? 1u : 0u;
+    const uint32_t q = p - h * HALF;
+    r = q / ROWW;
+    c = q - r * ROWW;
+  }
+  // shared word -> canonical cube word (L >= 5, data words only)
   __device__ static uint32_t canon(uint32_t p) {
     if constexpr (!skew) return p;
-    const uint32_t r = p / ROWW, c = p - r * ROWW;
-    return r * (ROWW - 1) + c;
+    uint32_t h, r, c;
+    locate(p, h, r, c);
+    if constexpr (split) return (r << 7) | (c << 1) | h;
+    else return r * (GW << L) + c;
   }
   // bit mask that records B' (= bsel mod 2^L) in a shared word
   __device__ static uint32_t set_mask(uint32_t bsel) {
@@ -189,18 +224,25 @@ struct Smem {
     else return REP << (bsel & ((1u << L) - 1u));
   }
 };
+// layout of the build kernel's bitset, and of the classify operand
+template <int L>
+using Smem = SmemT<L, true>;
+template <int L>
+using SmemC = SmemT<L, false>;
 
 // Shared row-layout word p of the classify operand, from the canonical cube.
-template <int L>
+template <class LY>
 __device__ __forceinline__ uint32_t smem_word_from_cube(const uint32_t* __restrict__ cube, uint32_t p) {
-  const uint32_t r = p / Smem<L>::ROWW, c = p - r * Smem<L>::ROWW;
-  if (c == Smem<L>::ROWW - 1) return 0u;                               // pad
+  constexpr int L = LY::L;
+  uint32_t h, r, c;
+  LY::locate(p, h, r, c);
+  if (c >= (LY::GW << L) || r >= (1u << L)) return 0u;                 // pad / hole
   if constexpr (L >= 5) {
-    return __ldg(cube + r * (Smem<L>::ROWW - 1) + c);
+    return __ldg(cube + LY::canon(p));
   } else {
     const uint32_t idx = (r << (2 * L)) | (c << L);
-    const uint32_t row = (__ldg(cube + (idx >> 5)) >> (idx & 31u)) & Smem<L>::ROWMASK;
-    return row * Smem<L>::REP;
+    const uint32_t row = (__ldg(cube + (idx >> 5)) >> (idx & 31u)) & LY::ROWMASK;
+    return row * LY::REP;
   }
 }
 
@@ -216,20 +258,26 @@ __device__ __forceinline__ void flush_smem_word(uint32_t* __restrict__ dst, uint
   }
 }
 
-// Skewed-layout byte address and bit selector of pixel x = [*, G, B, R].
-// `obase` (optional) is a shared-window base with its low 9 bits clear: it is
-// OR-ed into the in-row offset at no cost instead of a separate add.
-template <int L>
+// Row-layout byte address and bit selector of pixel x = [*, G, B, R].
+// `obase` (optional, L <= 5) is a shared-window base with its low 9 bits
+// clear: it is OR-ed into the in-row offset instead of a separate add.
+template <class LY>
 __device__ __forceinline__ void skew_lookup(uint32_t x, uint32_t& addr, uint32_t& bsel, uint32_t obase = 0) {
+  constexpr int L = LY::L;
   constexpr int s = 8 - L;
-  constexpr int gpos = (L > 5 ? L - 5 : 0) + 2;                     // byte-address bit of G' lsb
-  constexpr int gsh = 16 - L - gpos;                                // G' lsb sits at x bit 16-L
   const uint32_t r = __umulhi(x, 1u << (8 - s));                    // x >> (24+s) = R'
   bsel = __umulhi(x, 1u << (16 - s));                               // x >> (16+s): low bits = B'
-  const uint32_t g = __umulhi(x, 1u << (32 - gsh));                 // G' at bit gpos
-  uint32_t c = (g & (((1u << L) - 1u) << gpos)) | obase;
-  if constexpr (L == 6) c |= __umulhi(x, 1u << (5 + L)) & 4u;        // x >> (27-L): B'5 at bit 2
-  addr = r * (Smem<L>::ROWW * 4u) + c;
+  uint32_t c;
+  if constexpr (LY::split) {
+    c = (__umulhi(x, 1u << 24) & 0x80FCu) + obase;                  // G & 0xFC | (B & 0x80) << 8
+  } else {
+    constexpr int gpos = (L > 5 ? L - 5 : 0) + 2;                   // byte-address bit of G' lsb
+    constexpr int gsh = 16 - L - gpos;                              // G' lsb sits at x bit 16-L
+    const uint32_t g = __umulhi(x, 1u << (32 - gsh));               // G' at bit gpos
+    c = (g & (((1u << L) - 1u) << gpos)) | obase;
+    if constexpr (L == 6) c |= __umulhi(x, 1u << (5 + L)) & 4u;      // x >> (27-L): B'5 at bit 2
+  }
+  addr = r * (LY::ROWW * 4u) + c;
 }
 
 // Pixel j (0..15) of a 48-byte unit held in w[0..11] -> [*, R, G, B]
@@ -345,10 +393,10 @@ __device__ __forceinline__ uint32_t operand_to_cube(uint32_t x) {
 
 // Word byte address + bit selector of operand x in the leaf bitset `bits`
 // (shared for L <= 6, global cube for L >= 7).
-template <int L>
+template <int L, class LY = Smem<L>>
 __device__ __forceinline__ void bit_position(uint32_t x, uint32_t& addr, uint32_t& bsel, uint32_t obase = 0) {
-  if constexpr (Smem<L>::skew) {
-    skew_lookup<L>(x, addr, bsel, obase);
+  if constexpr (LY::skew) {
+    skew_lookup<LY>(x, addr, bsel, obase);
   } else {
     const uint32_t idx = cube_idx<L>(x);
     addr = ((idx >> 5) << 2) + obase;
@@ -358,51 +406,62 @@ __device__ __forceinline__ void bit_position(uint32_t x, uint32_t& addr, uint32_
 
 // Shared-layout addresses of pixels 2K and 2K+1 of a unit, two at a time:
 // every address is < 64 KB, so both pixels ride in the 16-bit halves of one
-// register through one IMAD (R' x row stride + in-row offset) -- about 6.5
+// register through one IMAD (R' x row stride + in-row offset) -- about 6
 // pipe instructions per pixel instead of 10 for one-at-a-time extraction.
 //   yR = [R_A, *, R_B, *]   yG = [G_A, B_A, G_B, B_B]   (two PRMTs, bytes of
 // the pair lie in one 8-byte window of the unit since 6K mod 4 is 0 or 2)
-// `obase2` = shared base replicated in both halves (base < 32 KB... the sum
-// of base and offset must stay below 64 KB).
-template <int L, int K>
+// For L = 6 (split layout) the in-row offsets of both pixels are one mask of
+// yG.  The low half is split off with an IMAD (FMA pipe) rather than a mask:
+// the ALU pipe carries the permutes, masks and funnel shifts and is the
+// busier of the two (ncu r10: ALU 56 %, FMA 16 %).
+// `obase2` = shared base replicated in both halves (L <= 5 only; the sum of
+// base and offset must stay below 64 KB).  Callers that read through a
+// shared pointer pass 0 and let the LDS add the base.
+template <class LY, int K>
 __device__ __forceinline__ void pair_positions(const uint32_t (&w)[12], uint32_t obase2, uint32_t& addr_a,
                                                uint32_t& bsel_a, uint32_t& addr_b, uint32_t& bsel_b) {
-  static_assert(Smem<L>::skew, "pair_positions needs the shared row layout");
+  constexpr int L = LY::L;
+  static_assert(LY::skew, "pair_positions needs the shared row layout");
   constexpr int o = 6 * K, a = o >> 2, b = o & 3;
   constexpr int s = 8 - L;
-  constexpr int gpos = (L > 5 ? L - 5 : 0) + 2;                     // byte-address bit of G' lsb
   constexpr uint32_t M = (1u << L) - 1u;
   constexpr uint32_t selR = uint32_t(b) | (uint32_t(b) << 4) | (uint32_t(b + 3) << 8) | (uint32_t(b + 3) << 12);
   constexpr uint32_t selG = uint32_t(b + 1) | (uint32_t(b + 2) << 4) | (uint32_t(b + 4) << 8) | (uint32_t(b + 5) << 12);
   const uint32_t yR = __byte_perm(w[a], w[a + 1], selR);
   const uint32_t yG = __byte_perm(w[a], w[a + 1], selG);
   const uint32_t P = __umulhi(yR, 1u << (32 - s)) & (M | (M << 16));           // R'_A | R'_B << 16
-  uint32_t g;
-  if constexpr (gpos >= s) g = yG << (gpos - s);                                 // G' at gpos in each half
-  else g = __umulhi(yG, 1u << (32 - (s - gpos)));
-  uint32_t t = obase2;                                                           // base in both halves
-  if constexpr (L == 6) t |= __umulhi(yG, 1u << 19) & 0x00040004u;             // B'5 (bits 15, 31) -> 2, 18
-  const uint32_t q = (g & ((M << gpos) | (M << (gpos + 16)))) | t;
-  const uint32_t pair = P * (Smem<L>::ROWW * 4u) + q;
-  addr_a = pair & 0xFFFFu;
+  uint32_t q;
+  if constexpr (LY::split) {
+    q = (yG & 0x80FC80FCu) | obase2;                                             // G & 0xFC | (B & 0x80) << 8
+  } else {
+    constexpr int gpos = (L > 5 ? L - 5 : 0) + 2;                                // byte-address bit of G' lsb
+    uint32_t g;
+    if constexpr (gpos >= s) g = yG << (gpos - s);                               // G' at gpos in each half
+    else g = __umulhi(yG, 1u << (32 - (s - gpos)));
+    uint32_t t = obase2;
+    if constexpr (L == 6) t |= __umulhi(yG, 1u << 19) & 0x00040004u;           // B'5 (bits 15, 31) -> 2, 18
+    q = (g & ((M << gpos) | (M << (gpos + 16)))) | t;
+  }
+  const uint32_t pair = P * (LY::ROWW * 4u) + q;
   addr_b = __umulhi(pair, 1u << 16);
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(addr_a) : "r"(addr_b), "r"(0xFFFF0000u), "r"(pair));   // pair & 0xFFFF
   bsel_a = __umulhi(yG, 1u << (24 - s));                                         // B_A' in the low bits
   bsel_b = __umulhi(yG, 1u << (8 - s));                                          // B_B'
 }
 
 // pair_positions with a pair index known after unrolling
-template <int L>
+template <class LY>
 __device__ __forceinline__ void pair_positions_dyn(const uint32_t (&w)[12], int k, uint32_t obase2, uint32_t& aa,
                                                    uint32_t& ba, uint32_t& ab, uint32_t& bb) {
   switch (k) {
-    case 0: pair_positions<L, 0>(w, obase2, aa, ba, ab, bb); break;
-    case 1: pair_positions<L, 1>(w, obase2, aa, ba, ab, bb); break;
-    case 2: pair_positions<L, 2>(w, obase2, aa, ba, ab, bb); break;
-    case 3: pair_positions<L, 3>(w, obase2, aa, ba, ab, bb); break;
-    case 4: pair_positions<L, 4>(w, obase2, aa, ba, ab, bb); break;
-    case 5: pair_positions<L, 5>(w, obase2, aa, ba, ab, bb); break;
-    case 6: pair_positions<L, 6>(w, obase2, aa, ba, ab, bb); break;
-    default: pair_positions<L, 7>(w, obase2, aa, ba, ab, bb); break;
+    case 0: pair_positions<LY, 0>(w, obase2, aa, ba, ab, bb); break;
+    case 1: pair_positions<LY, 1>(w, obase2, aa, ba, ab, bb); break;
+    case 2: pair_positions<LY, 2>(w, obase2, aa, ba, ab, bb); break;
+    case 3: pair_positions<LY, 3>(w, obase2, aa, ba, ab, bb); break;
+    case 4: pair_positions<LY, 4>(w, obase2, aa, ba, ab, bb); break;
+    case 5: pair_positions<LY, 5>(w, obase2, aa, ba, ab, bb); break;
+    case 6: pair_positions<LY, 6>(w, obase2, aa, ba, ab, bb); break;
+    default: pair_positions<LY, 7>(w, obase2, aa, ba, ab, bb); break;
   }
 }
 
@@ -412,58 +471,74 @@ __device__ __forceinline__ void unpack16(const uint32_t (&w)[12], uint32_t (&px)
   if constexpr (J + 1 < 16) unpack16<J + 1, L>(w, px);
 }
 
+// Shared-window address of the build kernel's dynamic shared memory: the
+// kernel has no static shared variables and is launched without clusters,
+// so its dynamic block starts right after the 1 KB reserved per CTA.  The
+// kernel checks this once (trap otherwise); in exchange every lookup and
+// atomic is [offset + immediate] -- a materialised base register costs an
+// extra IADD per pixel.
+constexpr uint32_t DYN_SMEM_BASE = 1024u;
+__device__ __forceinline__ uint32_t lds_at(uint32_t off) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1+1024];" : "=r"(v) : "r"(off));
+  return v;
+}
+__device__ __forceinline__ void reds_or_at(uint32_t off, uint32_t v) {
+  asm volatile("red.shared.or.b32 [%0+1024], %1;" :: "r"(off), "r"(v) : "memory");
+}
+
 // One 16-pixel unit, called by all 32 lanes of a warp (`valid` false for
 // lanes past the segment).  Lookups go in groups of four; a group takes the
 // atomic path only if some lane of the warp misses one of its pixels -- a
 // warp-uniform branch, so the common path has no divergence (ncu r4-r6:
 // per-pixel divergent branches cost ~5 instructions/pixel).  About 0.45 % of
 // pixels miss at C3 (first occurrences of a colour within a CTA's range).
-
-__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
-  uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ void reds_or(uint32_t a, uint32_t v) {
-  asm volatile("red.shared.or.b32 [%0], %1;" :: "r"(a), "r"(v) : "memory");
-}
-
-// `sbase` = 32-bit shared-window address of the static, 1 KB-aligned bitset,
-// merged into the lookup address by bit_position (no per-pixel add);
-// `bits` = global bitset for L >= 7.
-template <int L, bool SMEM_BITS, bool COUNTS>
-__device__ __forceinline__ void build_unit(const uint32_t (&w)[12], uint32_t* bits, uint32_t sbase, uint32_t* cnt,
-                                           bool valid) {
+template <int L, bool SMEM_BITS, bool COUNTS, bool FULL>
+__device__ __forceinline__ void build_unit(const uint32_t (&w)[12], uint32_t* bits, uint32_t* cnt,
+                                           bool valid_, uint32_t dummy) {
+  // FULL: every lane of the warp holds a unit (the steady state); the tail
+  // variant carries per-lane `valid`
+  const bool valid = FULL || valid_;
   uint32_t px[16];
   unpack16<0, L>(w, px);
   char* base = reinterpret_cast<char*>(bits);
-  const uint32_t sbase2 = sbase | (sbase << 16);
 #pragma unroll
   for (int g = 0; g < 16; g += 4) {
     uint32_t addr[4], bsel[4], v[4];
     if constexpr (SMEM_BITS) {
-      pair_positions_dyn<L>(w, g / 2, sbase2, addr[0], bsel[0], addr[1], bsel[1]);
-      pair_positions_dyn<L>(w, g / 2 + 1, sbase2, addr[2], bsel[2], addr[3], bsel[3]);
+      // byte offsets; the shared base rides in the LDS address ([R+UR])
+      pair_positions_dyn<Smem<L>>(w, g / 2, 0u, addr[0], bsel[0], addr[1], bsel[1]);
+      pair_positions_dyn<Smem<L>>(w, g / 2 + 1, 0u, addr[2], bsel[2], addr[3], bsel[3]);
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       uint32_t wd;
       if constexpr (SMEM_BITS) {
-        wd = lds_u32(addr[j]);
+        wd = lds_at(addr[j]);
       } else {
         bit_position<L>(px[g + j], addr[j], bsel[j], 0u);
         wd = *reinterpret_cast<volatile uint32_t*>(base + addr[j]);
       }
       v[j] = __funnelshift_r(wd, wd, bsel[j]);
     }
-    const bool miss = valid && !(v[0] & v[1] & v[2] & v[3] & 1u);
-    if (__any_sync(0xFFFFFFFFu, miss)) {
+    if constexpr (SMEM_BITS) {
+      // warp-uniform skip; otherwise every lane issues four atomics, those
+      // of pixels that did not miss aimed at the lane's private dummy word:
+      // no per-lane branches or convergence barriers around the rare path
+      const bool miss = valid && !(v[0] & v[1] & v[2] & v[3] & 1u);
+      if (__any_sync(0xFFFFFFFFu, miss)) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (valid && !(v[j] & 1u)) {
-          if constexpr (SMEM_BITS) reds_or(addr[j], Smem<L>::set_mask(bsel[j]));
-          else atomicOr(reinterpret_cast<uint32_t*>(base + addr[j]), 1u << (bsel[j] & 31u));
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t o = (valid && !(v[j] & 1u)) ? addr[j] : dummy;
+          reds_or_at(o, Smem<L>::set_mask(bsel[j]));
         }
+      }
+    } else {
+      const bool miss = valid && !(v[0] & v[1] & v[2] & v[3] & 1u);
+      if (__any_sync(0xFFFFFFFFu, miss)) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (valid && !(v[j] & 1u)) atomicOr(reinterpret_cast<uint32_t*>(base + addr[j]), 1u << (bsel[j] & 31u));
       }
     }
   }
@@ -481,10 +556,12 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
              int group_size, int64_t units_per_cta, uint32_t* __restrict__ ws,
              uint32_t* __restrict__ out_pyr, int64_t n_trees, uint32_t* __restrict__ zero_cube,
              int64_t zero_words, uint32_t* __restrict__ counts) {
-  // static shared array: its address is a compile-time constant, so the
-  // lookups and atomics use [reg + imm] addressing (no per-pixel base add)
-  __shared__ __align__(1024) uint32_t s_bits[SMEM_BITS ? Smem<L>::words : 1];
-  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(s_bits));
+  // Smem<L>::alloc_words of dynamic shared memory (the bitset and the
+  // per-lane dummy words); lookups address it as [offset + UR base]
+  extern __shared__ __align__(1024) uint32_t s_bits[];
+  if constexpr (SMEM_BITS) {
+    if (static_cast<uint32_t>(__cvta_generic_to_shared(s_bits)) != DYN_SMEM_BASE) __trap();
+  }
   constexpr int64_t CW = cube_words(L);
   if (blockIdx.x == 0) {
     clear_shared_words(out_pyr, n_trees, L);
@@ -494,7 +571,7 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
   const int64_t u_end = min(total_units, u_begin + units_per_cta);
   if (u_begin >= u_end) return;
   if constexpr (SMEM_BITS) {
-    for (int i = threadIdx.x; i < Smem<L>::words; i += BUILD_BLOCK) s_bits[i] = 0u;
+    for (uint32_t i = threadIdx.x; i < Smem<L>::compact; i += BUILD_BLOCK) s_bits[Smem<L>::compact_word(i)] = 0u;
     __syncthreads();
   }
   const int64_t units_per_tree = units_per_frame * group_size;
@@ -506,18 +583,31 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
     if constexpr (SMEM_BITS) bits = s_bits;
     else bits = ws + tree * CW;
     uint32_t* cnt = COUNTS ? counts + tree * (int64_t(1) << (3 * L)) : nullptr;
-    // Two units per thread and iteration (six 16-byte loads in flight).  The
-    // trip count is warp-uniform (lanes past the segment carry valid=false) so
-    // that build_unit can branch on warp votes.
+    // Software-pipelined: the next unit's three 16-byte loads are in flight
+    // while the current one is looked up (unrolled by two so the buffers
+    // swap by renaming).  Trip counts are warp-uniform (lanes past the
+    // segment carry valid=false) so build_unit can branch on warp votes.
     const int lane = threadIdx.x & 31;
-    for (int64_t wv = u + threadIdx.x - lane; wv < seg_end; wv += 2 * BUILD_BLOCK) {
-      const int64_t v = wv + lane;
-      const bool first = v < seg_end, second = v + BUILD_BLOCK < seg_end;
-      uint32_t wa[12], wb[12];
-      if (first) load_unit(frames, v, wa);
-      if (second) load_unit(frames, v + BUILD_BLOCK, wb);
-      build_unit<L, SMEM_BITS, COUNTS>(wa, bits, sbase, cnt, first);
-      if (__any_sync(0xFFFFFFFFu, second)) build_unit<L, SMEM_BITS, COUNTS>(wb, bits, sbase, cnt, second);
+    const uint32_t dummy = 4u * (Smem<L>::DUMMY + uint32_t(lane));   // byte offset
+    int64_t wv = u + threadIdx.x - lane;
+    uint32_t wa[12], wb[12];
+    if (wv + lane < seg_end) load_unit(frames, wv + lane, wa);
+    while (wv < seg_end) {
+      {
+        const int64_t wn = wv + BUILD_BLOCK;
+        if (wn + lane < seg_end) load_unit(frames, wn + lane, wb);
+        if (wv + 32 <= seg_end) build_unit<L, SMEM_BITS, COUNTS, true>(wa, bits, cnt, true, dummy);
+        else build_unit<L, SMEM_BITS, COUNTS, false>(wa, bits, cnt, wv + lane < seg_end, dummy);
+        wv = wn;
+      }
+      if (wv >= seg_end) break;
+      {
+        const int64_t wn = wv + BUILD_BLOCK;
+        if (wn + lane < seg_end) load_unit(frames, wn + lane, wa);
+        if (wv + 32 <= seg_end) build_unit<L, SMEM_BITS, COUNTS, true>(wb, bits, cnt, true, dummy);
+        else build_unit<L, SMEM_BITS, COUNTS, false>(wb, bits, cnt, wv + lane < seg_end, dummy);
+        wv = wn;
+      }
     }
     if constexpr (SMEM_BITS) {
       // OR the CTA's non-zero words into the tree's cube bitset.  (Converting
@@ -525,9 +615,10 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
       // ~4.6 CTA segments at C3 -- ncu r8.)
       __syncthreads();
       uint32_t* dst = ws + tree * CW;
-      for (int i = threadIdx.x; i < Smem<L>::words; i += BUILD_BLOCK) {
-        const uint32_t x = s_bits[i];
-        if (x) { flush_smem_word<L>(dst, uint32_t(i), x); s_bits[i] = 0u; }   // pad words stay 0
+      for (uint32_t i = threadIdx.x; i < Smem<L>::compact; i += BUILD_BLOCK) {
+        const uint32_t p = Smem<L>::compact_word(i);
+        const uint32_t x = s_bits[p];
+        if (x) { flush_smem_word<L>(dst, p, x); s_bits[p] = 0u; }   // pad words stay 0
       }
       __syncthreads();
     }
@@ -944,7 +1035,7 @@ __device__ __forceinline__ void classify_unit(const uint32_t (&w)[12], const uin
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       uint32_t aa, ba, ab, bb;
-      pair_positions_dyn<L>(w, k, 0u, aa, ba, ab, bb);
+      pair_positions_dyn<SmemC<L>>(w, k, 0u, aa, ba, ab, bb);
       const uint32_t wa = *reinterpret_cast<const uint32_t*>(base + aa);
       const uint32_t wb = *reinterpret_cast<const uint32_t*>(base + ab);
       v[2 * k] = __funnelshift_r(wa, wa, ba);                       // bit 0 = background
@@ -956,7 +1047,7 @@ __device__ __forceinline__ void classify_unit(const uint32_t (&w)[12], const uin
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       uint32_t addr, bsel;
-      bit_position<L>(px[j], addr, bsel);
+      bit_position<L, SmemC<L>>(px[j], addr, bsel);
       const uint32_t wd = __ldg(reinterpret_cast<const uint32_t*>(base + addr));
       v[j] = __funnelshift_r(wd, wd, bsel);
     }
@@ -972,7 +1063,10 @@ k_classify_flat(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_p
   constexpr int64_t CW = cube_words(L);
   const uint32_t* bits = cube;
   if constexpr (SMEM_BITS) {
-    for (int i = threadIdx.x; i < Smem<L>::words; i += CLS_BLOCK) s_bits[i] = smem_word_from_cube<L>(cube, i);
+    for (uint32_t i = threadIdx.x; i < SmemC<L>::compact; i += CLS_BLOCK) {
+      const uint32_t p = SmemC<L>::compact_word(i);
+      s_bits[p] = smem_word_from_cube<SmemC<L>>(cube, p);
+    }
     __syncthreads();
     bits = s_bits;
   }
@@ -992,7 +1086,7 @@ k_classify_flat(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_p
       for (int64_t i = n_units * 16 + threadIdx.x; i < n_pixels; i += CLS_BLOCK) {
         const uint32_t x = Smem<L>::skew ? gbr_word_scalar(frames + 3 * i) : rgb_word_scalar(frames + 3 * i);
         uint32_t addr, bsel;
-        bit_position<L>(x, addr, bsel);
+        bit_position<L, SmemC<L>>(x, addr, bsel);
         const uint32_t* wp = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(bits) + addr);
         const uint32_t wd = SMEM_BITS ? *wp : __ldg(wp);
         mask[i] = uint8_t(((wd >> (bsel & 31u)) & 1u) ^ 1u);
@@ -1245,16 +1339,18 @@ static int launch_build_flat(const uint8_t* frames, int64_t units_per_frame, int
                              uint32_t* ws, uint32_t* out_pyr, int64_t n_trees, uint32_t* zero_cube, int64_t zero_words,
                              uint32_t* counts, cudaStream_t st) {
   constexpr bool SMEM = L <= 6;
-  const size_t smem = 0;   // the bitset is a static __shared__ array
+  const size_t smem = SMEM ? size_t(Smem<L>::alloc_words) * 4 : 0;
   // one-time per instantiation: opt in to > 48 KB dynamic smem, cache occupancy
   static int occ[2] = {0, 0};
   int& blocks_per_sm = occ[counts ? 1 : 0];
   if (blocks_per_sm == 0) {
     if (counts) {
       auto k = k_build_flat<L, SMEM, true>;
+      CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       blocks_per_sm = occupancy(k, BUILD_BLOCK, smem);
     } else {
       auto k = k_build_flat<L, SMEM, false>;
+      CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       blocks_per_sm = occupancy(k, BUILD_BLOCK, smem);
     }
   }
@@ -1467,12 +1563,21 @@ template <int L>
 static int launch_classify_flat(const uint8_t* frames, int64_t n_pixels, const uint32_t* cube, uint8_t* mask,
                                 bool packed, cudaStream_t st) {
   constexpr bool SMEM = L <= 6;
-  const size_t smem = SMEM ? size_t(Smem<L>::words) * 4 : 0;
+  const size_t smem = SMEM ? size_t(SmemC<L>::words) * 4 : 0;
   const int64_t n_units = n_pixels / 16;
   static int occ[2] = {0, 0};
   int& bps = occ[packed ? 1 : 0];
-  if (bps == 0) bps = packed ? occupancy(k_classify_flat<L, SMEM, true>, CLS_BLOCK, smem)
-                             : occupancy(k_classify_flat<L, SMEM, false>, CLS_BLOCK, smem);
+  if (bps == 0) {
+    if (packed) {
+      CUDA_TRY(cudaFuncSetAttribute(k_classify_flat<L, SMEM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(smem)));
+      bps = occupancy(k_classify_flat<L, SMEM, true>, CLS_BLOCK, smem);
+    } else {
+      CUDA_TRY(cudaFuncSetAttribute(k_classify_flat<L, SMEM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(smem)));
+      bps = occupancy(k_classify_flat<L, SMEM, false>, CLS_BLOCK, smem);
+    }
+  }
   int64_t grid = int64_t(sm_count()) * bps;
   const int64_t need = (n_units + CLS_BLOCK - 1) / CLS_BLOCK;
   if (grid > need) grid = need;
