@@ -76,6 +76,13 @@ __host__ __device__ static constexpr int64_t operand_words(int L) {
   return cube_words(L) + (L == 7 ? S7_CANON_WORDS : 0);
 }
 
+// Build workspace per tree: the leaf cube, then levels 1..L-1 in cube order
+// (obg_build_model; obg_build_presence leaves the upper part zero), padded to
+// 128 bytes so every tree's cube is 16-byte aligned.
+__host__ __device__ static constexpr int64_t ws_words(int L) {
+  return cube_words(L) + ((level_offset(L) + 31) / 32) * 32;
+}
+
 constexpr int PYR_CHUNK = 1024;  // k_pyramid: leaf-level words per CTA (a 32x32x32 sub-cube)
 
 // Leading words of a pyramid (levels 1..z) that k_pyramid ORs in with atomics
@@ -194,8 +201,11 @@ struct SmemT {
   static constexpr uint32_t compact = split ? 2u * ROWS : uint32_t(words);
   // first of 32 per-lane dummy words (build kernel atomics that must not land)
   static constexpr uint32_t DUMMY = split ? ROWS : uint32_t(words);
-  static constexpr int64_t alloc_words = split ? words : words + 32;
-  static_assert(!split || ROWS + 32 <= HALF, "split halves overlap");
+  // build kernel: cube-order levels 1..L-1 of a flushed segment (level_offset
+  // layout); in the hole when split
+  static constexpr uint32_t SCRATCH = DUMMY + 32;
+  static constexpr int64_t alloc_words = split ? words : words + 32 + level_offset(L);
+  static_assert(!split || ROWS + 32 + level_offset(L) <= HALF, "split halves overlap");
   static constexpr uint32_t REP = L >= 5 ? 1u : L == 4 ? 0x00010001u : L == 3 ? 0x01010101u
                                   : L == 2 ? 0x11111111u : 0x55555555u;
   // the 2^L-bit B' row of an L <= 4 word
@@ -471,6 +481,87 @@ __device__ __forceinline__ void unpack16(const uint32_t (&w)[12], uint32_t (&px)
   if constexpr (J + 1 < 16) unpack16<J + 1, L>(w, px);
 }
 
+// bit i = bit 2i | bit 2i+1 of x (16 bits out of 32)
+__device__ __forceinline__ uint32_t fold_pairs(uint32_t x) {
+  x = (x | (x >> 1)) & 0x55555555u;
+  x = (x | (x >> 1)) & 0x33333333u;
+  x = (x | (x >> 2)) & 0x0F0F0F0Fu;
+  x = (x | (x >> 4)) & 0x00FF00FFu;
+  x = (x | (x >> 8)) & 0x0000FFFFu;
+  return x;
+}
+
+// Word pw of cube-order level l (side m = 2^l, bit (r<<2l | g<<l | b)) from
+// cube-order level l+1 `child` (side 2m).
+__device__ __forceinline__ uint32_t reduce_cube_word(const uint32_t* child, int l, uint32_t pw) {
+  if (l >= 5) {
+    // the word is 32 bits of one parent row (r, g); the row's 2m-bit child
+    // rows (2r+dr, 2g+dg) hold it in words 2k, 2k+1
+    const uint32_t k = pw & ((1u << (l - 5)) - 1u), row = pw >> (l - 5);
+    const uint32_t r = row >> l, g = row & ((1u << l) - 1u);
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      const uint32_t R = 2 * r + (d >> 1), G = 2 * g + (d & 1);
+      const uint32_t w0 = (((R << (l + 1)) + G) << (l - 4)) + 2 * k;
+      lo |= child[w0];
+      hi |= child[w0 + 1];
+    }
+    return fold_pairs(lo) | (fold_pairs(hi) << 16);
+  }
+  // l <= 4: the word holds 32/m parent rows of m bits (fewer for l = 1)
+  const uint32_t m = 1u << l;
+  const uint32_t rows = min(32u / m, (1u << (3 * l)) / m);
+  const uint32_t cmask = (2 * m >= 32) ? 0xFFFFFFFFu : ((1u << (2 * m)) - 1u);
+  uint32_t out = 0;
+  for (uint32_t j = 0; j < rows; ++j) {
+    const uint32_t row = ((32u * pw) >> l) + j;
+    const uint32_t r = row >> l, g = row & (m - 1u);
+    uint32_t acc = 0;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      const uint32_t R = 2 * r + (d >> 1), G = 2 * g + (d & 1);
+      const uint32_t off = ((R << (l + 1)) + G) * (2 * m);
+      acc |= (child[off >> 5] >> (off & 31u)) & cmask;
+    }
+    out |= fold_pairs(acc) << (j * m);
+  }
+  return out;
+}
+
+// Word pw of cube-order level L-1 from the build kernel's row-layout bitset
+// (the child rows (2r+dr, 2g+dg) of each parent row, OR-ed and pair-folded as
+// in reduce_cube_word).
+template <int L>
+__device__ __forceinline__ uint32_t level_below_from_smem(const uint32_t* s, uint32_t pw) {
+  using S = Smem<L>;
+  if constexpr (L == 6) {
+    const uint32_t r = pw >> 5, g = pw & 31u;     // one level-5 row per word
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      const uint32_t a = (2 * r + (d >> 1)) * S::ROWW + 2 * g + (d & 1);
+      lo |= s[a];
+      hi |= s[S::HALF + a];
+    }
+    return fold_pairs(lo) | (fold_pairs(hi) << 16);
+  } else {
+    constexpr uint32_t m = 1u << (L - 1);                       // parent row bits
+    constexpr uint32_t rows = (32u / m) < m * m ? 32u / m : m * m;
+    uint32_t out = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < rows; ++j) {
+      const uint32_t row = pw * (32u / m) + j;
+      const uint32_t r = row / m, g = row % m;
+      uint32_t acc = 0;
+#pragma unroll
+      for (int d = 0; d < 4; ++d) acc |= s[(2 * r + (d >> 1)) * S::ROWW + 2 * g + (d & 1)];
+      out |= fold_pairs(acc & S::ROWMASK) << (j * m);
+    }
+    return out;
+  }
+}
+
 // Shared-window address of the build kernel's dynamic shared memory: the
 // kernel has no static shared variables and is launched without clusters,
 // so its dynamic block starts right after the 1 KB reserved per CTA.  The
@@ -555,14 +646,14 @@ __global__ void __launch_bounds__(BUILD_BLOCK, 2)
 k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t total_units,
              int group_size, int64_t units_per_cta, uint32_t* __restrict__ ws,
              uint32_t* __restrict__ out_pyr, int64_t n_trees, uint32_t* __restrict__ zero_cube,
-             int64_t zero_words, uint32_t* __restrict__ counts) {
+             int64_t zero_words, uint32_t* __restrict__ counts, int levels_out) {
   // Smem<L>::alloc_words of dynamic shared memory (the bitset and the
   // per-lane dummy words); lookups address it as [offset + UR base]
   extern __shared__ __align__(1024) uint32_t s_bits[];
   if constexpr (SMEM_BITS) {
     if (static_cast<uint32_t>(__cvta_generic_to_shared(s_bits)) != DYN_SMEM_BASE) __trap();
   }
-  constexpr int64_t CW = cube_words(L);
+  constexpr int64_t CW = cube_words(L), WSW = ws_words(L);
   if (blockIdx.x == 0) {
     clear_shared_words(out_pyr, n_trees, L);
     for (int64_t i = threadIdx.x; i < zero_words; i += BUILD_BLOCK) zero_cube[i] = 0u;
@@ -581,7 +672,7 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
     const int64_t seg_end = min(u_end, (tree + 1) * units_per_tree);
     uint32_t* bits;
     if constexpr (SMEM_BITS) bits = s_bits;
-    else bits = ws + tree * CW;
+    else bits = ws + tree * WSW;
     uint32_t* cnt = COUNTS ? counts + tree * (int64_t(1) << (3 * L)) : nullptr;
     // Software-pipelined: the next unit's three 16-byte loads are in flight
     // while the current one is looked up (unrolled by two so the buffers
@@ -592,6 +683,19 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
     int64_t wv = u + threadIdx.x - lane;
     uint32_t wa[12], wb[12];
     if (wv + lane < seg_end) load_unit(frames, wv + lane, wa);
+#if defined(OBG_EXP) && OBG_EXP == 1
+    // experiment: lookups only (no frame traffic after the first unit)
+    for (; wv < seg_end; wv += BUILD_BLOCK) build_unit<L, SMEM_BITS, COUNTS, true>(wa, bits, cnt, true, dummy);
+#elif defined(OBG_EXP) && OBG_EXP == 2
+    // experiment: frame traffic only
+    uint32_t acc = 0;
+    for (; wv < seg_end; wv += BUILD_BLOCK) {
+      if (wv + lane < seg_end) load_unit(frames, wv + lane, wb);
+#pragma unroll
+      for (int i = 0; i < 12; ++i) acc ^= wb[i];
+    }
+    if (acc == 0x12345678u) s_bits[0] = acc;
+#endif
     while (wv < seg_end) {
       {
         const int64_t wn = wv + BUILD_BLOCK;
@@ -610,16 +714,48 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
       }
     }
     if constexpr (SMEM_BITS) {
-      // OR the CTA's non-zero words into the tree's cube bitset.  (Converting
-      // to the path-order pyramid here instead costs 5.5x more: a tree spans
-      // ~4.6 CTA segments at C3 -- ncu r8.)
+      // OR the CTA's non-zero words into the tree's cube bitset and, for
+      // obg_build_model, its cube-order levels L-1..1 into the tree's upper
+      // levels (OR of partial presence = presence of the union, so segments
+      // of one tree combine with atomics).  Cube-order levels are a few
+      // instructions per word; path-order ones here cost 5.5x K1's flush
+      // (ncu r8), which is why those are made once, for the merged model.
       __syncthreads();
-      uint32_t* dst = ws + tree * CW;
+      uint32_t* dst = ws + tree * WSW;
       for (uint32_t i = threadIdx.x; i < Smem<L>::compact; i += BUILD_BLOCK) {
         const uint32_t p = Smem<L>::compact_word(i);
         const uint32_t x = s_bits[p];
-        if (x) { flush_smem_word<L>(dst, p, x); s_bits[p] = 0u; }   // pad words stay 0
+        if (x) flush_smem_word<L>(dst, p, x);
       }
+      if constexpr (L >= 2) {
+        if (levels_out) {
+          uint32_t* up = dst + CW;
+          uint32_t* sc = s_bits + Smem<L>::SCRATCH;
+          constexpr uint32_t NW = uint32_t(level_words(L - 1));
+          constexpr uint32_t OFF = uint32_t(level_offset(L - 1));
+          for (uint32_t pw = threadIdx.x; pw < NW; pw += BUILD_BLOCK) {
+            const uint32_t v = level_below_from_smem<L>(s_bits, pw);
+            sc[OFF + pw] = v;
+            if (v) atomicOr(up + OFF + pw, v);
+          }
+          __syncthreads();
+          for (int l = L - 2; l >= 1; --l) {
+            const uint32_t nw = uint32_t(level_words(l)), off = uint32_t(level_offset(l));
+            const uint32_t* child = sc + level_offset(l + 1);
+            for (uint32_t pw = threadIdx.x; pw < nw; pw += BUILD_BLOCK) {
+              const uint32_t v = reduce_cube_word(child, l, pw);
+              sc[off + pw] = v;
+              if (v) atomicOr(up + off + pw, v);
+            }
+            __syncthreads();
+          }
+        } else {
+          __syncthreads();
+        }
+      } else {
+        __syncthreads();
+      }
+      for (uint32_t i = threadIdx.x; i < Smem<L>::compact; i += BUILD_BLOCK) s_bits[Smem<L>::compact_word(i)] = 0u;
       __syncthreads();
     }
     u = seg_end;
@@ -652,7 +788,7 @@ k_build_generic(const uint8_t* __restrict__ frames, int64_t n_pixels_used, int H
     const uint8_t* px = frames + 3 * i;
     const uint32_t idx = ((uint32_t(px[0]) >> s) << (2 * L)) | ((uint32_t(px[1]) >> s) << L) |
                          ((uint32_t(px[2]) >> s) & m);
-    uint32_t* wp = ws + tree * CW + (idx >> 5);
+    uint32_t* wp = ws + tree * ws_words(L) + (idx >> 5);
     if (!((*reinterpret_cast<volatile uint32_t*>(wp) >> (idx & 31u)) & 1u)) atomicOr(wp, 1u << (idx & 31u));
     if (COUNTS) {
       uint32_t code = cube_to_code(idx, L);
@@ -924,6 +1060,187 @@ k_merge(const uint32_t* __restrict__ pyr, int n_trees, int n_regions, int L, int
       if (cube && w >= leaf_off) scatter_leaf_word_to_cube(bits, uint32_t(w - leaf_off), L, cube + r * operand_words(L));
     }
     __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Whole-model build (obg_build_model) in cube order.  The merge counts nodes
+// per (level, cell) and does not care how a level's bits are ordered, so the
+// per-tree levels stay in the cube order K1 produces: level l-1 from level l
+// is an OR over 2x2x2 blocks -- four rows OR-ed, then adjacent bit pairs
+// folded -- a few instructions per word instead of the 8 nibble gathers of
+// a path-order word (k_pyramid: 12.9 us at C3, ncu r9).  Only the merged
+// model (one tree per region) is converted to path order, and its leaf level
+// is already the classify operand.
+//   K2c k_levels_cube  per tree: levels L-1..1 (cube order) into the scratch
+//                      tree pyramids, from the workspace cube
+//   K3c k_merge_cube   per node word: count over trees, threshold; merged
+//                      leaf level -> the classify operand, merged upper levels
+//                      -> the scratch slot of group 0; workspace zeroed
+//   K4  k_morton_merged merged levels -> path-order pyramid (out_merged)
+// ---------------------------------------------------------------------------
+
+// Levels L-1 .. 1 of tree t (cube order) into the workspace after its leaf
+// cube, for the builds whose K1 has no shared-memory bitset (L >= 7, or the
+// generic multi-region / unaligned path); one CTA per tree.  Levels of <= 8192 words (l <= 6) are staged in
+// shared memory (ping-pong A/B), so the chain of levels costs one global
+// round trip (the leaf load) instead of one per level (ncu r11: 10 us).
+constexpr int LVL_BLOCK = 512;
+constexpr uint32_t LVL_A = 8192, LVL_B = 1024;
+__global__ void __launch_bounds__(LVL_BLOCK)
+k_levels_cube(uint32_t* __restrict__ ws, int L) {
+  __shared__ __align__(16) uint32_t s_a[LVL_A];
+  __shared__ __align__(16) uint32_t s_b[LVL_B];
+  const int64_t t = blockIdx.x;
+  const uint32_t* leaf = ws + t * ws_words(L);
+  uint32_t* o = ws + t * ws_words(L) + cube_words(L);   // upper levels, level_offset layout
+  const uint32_t* child;
+  uint32_t* cur = s_a;                             // smem buffer holding the child level (if staged)
+  bool staged = false;
+  if (L <= 6) {
+    const uint32_t n = uint32_t(cube_words(L));
+    if (n >= 4) {
+      for (uint32_t i = threadIdx.x; i < n / 4; i += LVL_BLOCK)
+        reinterpret_cast<uint4*>(s_a)[i] = __ldcg(reinterpret_cast<const uint4*>(leaf) + i);
+    } else if (threadIdx.x < n) {
+      s_a[threadIdx.x] = __ldcg(leaf + threadIdx.x);
+    }
+    __syncthreads();
+    staged = true;
+  }
+  for (int l = L - 1; l >= 1; --l) {
+    if (staged) child = cur;
+    else child = (l == L - 1) ? leaf : o + level_offset(l + 1);
+    uint32_t* parent = o + level_offset(l);
+    uint32_t* next = (cur == s_a) ? s_b : s_a;
+    const bool stage = l <= 6;                     // level fits the other buffer
+    const uint32_t nw = uint32_t(level_words(l));
+    for (uint32_t pw = threadIdx.x; pw < nw; pw += LVL_BLOCK) {
+      const uint32_t v = reduce_cube_word(child, l, pw);
+      parent[pw] = v;
+      if (stage) (staged ? next : s_a)[pw] = v;
+    }
+    if (stage) {
+      cur = staged ? next : s_a;
+      staged = true;
+    }
+    __syncthreads();   // level l complete (and visible to the CTA) before level l-1 reads it
+  }
+}
+
+// K3c.  Block = 32 node words (threadIdx.x) x MERGE_GROUPS_C tree groups, SWAR
+// byte counters as in k_merge; grid = (word blocks, regions).  Every tree
+// word comes from the workspace (leaf cube, then upper levels) and is zeroed
+// after reading.  Merged leaf words go to the classify operand, merged upper
+// words to `pyr` (region r at r * PW, level_offset layout) for K4.
+constexpr int MERGE_GROUPS_C = 16;
+__global__ void __launch_bounds__(32 * MERGE_GROUPS_C)
+k_merge_cube(uint32_t* __restrict__ pyr, uint32_t* __restrict__ ws, int n_groups, int n_regions, int L,
+             int64_t k_min, uint32_t* __restrict__ cube) {
+  const int64_t r = blockIdx.y;
+  __shared__ uint32_t s_acc[MERGE_GROUPS_C][8][32];
+  __shared__ uint32_t s_wide[32][33];
+  __shared__ uint32_t s_bits[MERGE_GROUPS_C][32];
+  const int x = threadIdx.x, y = threadIdx.y;
+  const int64_t PW = pyr_words(L), CW = cube_words(L), OW = operand_words(L), WSW = ws_words(L);
+  const int64_t leaf_off = level_offset(L);
+  const bool wide = (n_groups + MERGE_GROUPS_C - 1) / MERGE_GROUPS_C >= 252;   // a thread may flush
+  for (int64_t base = int64_t(blockIdx.x) * 32; base < PW; base += int64_t(gridDim.x) * 32) {
+    const int64_t w = base + x;
+    const bool valid = w < PW;
+    const bool leafw = w >= leaf_off;
+    if (wide) {
+      for (int i = y * 32 + x; i < 32 * 33; i += 32 * MERGE_GROUPS_C) (&s_wide[0][0])[i] = 0;
+      __syncthreads();
+    }
+    uint32_t acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0;
+    int since = 0;
+    if (valid) {
+      uint32_t* p = ws + r * WSW + (leafw ? w - leaf_off : CW + w);
+      const int64_t stride = WSW * n_regions;
+      int t = y;
+      for (; t + 3 * MERGE_GROUPS_C < n_groups; t += 4 * MERGE_GROUPS_C) {
+        uint32_t* pa = p + int64_t(t) * stride;
+        const int64_t st = int64_t(MERGE_GROUPS_C) * stride;
+        const uint32_t a = __ldcg(pa), b = __ldcg(pa + st), d = __ldcg(pa + 2 * st), e = __ldcg(pa + 3 * st);
+        // hand the workspace back zeroed
+        if (a) pa[0] = 0u;
+        if (b) pa[st] = 0u;
+        if (d) pa[2 * st] = 0u;
+        if (e) pa[3 * st] = 0u;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          acc[q] += ((a >> q) & 0x01010101u) + ((b >> q) & 0x01010101u) + ((d >> q) & 0x01010101u) +
+                    ((e >> q) & 0x01010101u);
+        since += 4;
+        if (since > 251) {   // keep byte counters below 256
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) atomicAdd(&s_wide[x][q + 8 * j], (acc[q] >> (8 * j)) & 0xFFu);
+            acc[q] = 0;
+          }
+          since = 0;
+        }
+      }
+      for (; t < n_groups; t += MERGE_GROUPS_C) {
+        uint32_t* pa = p + int64_t(t) * stride;
+        const uint32_t a = __ldcg(pa);
+        if (a) *pa = 0u;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] += (a >> q) & 0x01010101u;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s_acc[y][q][x] = acc[q];
+    __syncthreads();
+    // threads y < 8: bits y, y+8, y+16, y+24 of word x
+    if (y < 8) {
+      uint32_t c[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int g = 0; g < MERGE_GROUPS_C; ++g) {
+        const uint32_t v = s_acc[g][y][x];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[j] += (v >> (8 * j)) & 0xFFu;
+      }
+      if (wide) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[j] += s_wide[x][y + 8 * j];
+      }
+      uint32_t part = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) part |= uint32_t(int64_t(c[j]) >= k_min) << (y + 8 * j);
+      s_bits[y][x] = part;
+    }
+    __syncthreads();
+    if (y == 0 && valid) {
+      uint32_t bits = 0;
+#pragma unroll
+      for (int g = 0; g < 8; ++g) bits |= s_bits[g][x];
+      if (L == 1) bits &= 0xFFu;
+      if (leafw) cube[r * OW + (w - leaf_off)] = bits;
+      else pyr[r * PW + w] = bits;
+    }
+    __syncthreads();
+  }
+}
+
+// K4: merged path-order pyramid words from the merged cube-order levels
+// (levels < L in group 0's scratch slot, level L in the operand).
+__global__ void __launch_bounds__(256)
+k_morton_merged(const uint32_t* __restrict__ pyr, const uint32_t* __restrict__ cube, int n_regions, int L,
+                uint32_t* __restrict__ out) {
+  const int64_t PW = pyr_words(L), OW = operand_words(L);
+  const int64_t total = PW * n_regions;
+  for (int64_t wi = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; wi < total;
+       wi += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = wi / PW, w = wi - r * PW;
+    int l = 1;
+    while (l < L && w >= level_offset(l + 1)) ++l;
+    const uint32_t* src = (l == L) ? cube + r * OW : pyr + r * PW + level_offset(l);
+    out[wi] = morton_word_from_cube(src, uint32_t(w - level_offset(l)), l);
   }
 }
 
@@ -1320,7 +1637,7 @@ int64_t obg_level_offset(int levels, int level) {
 int64_t obg_cube_words(int levels) { return (levels < 1 || levels > 8) ? -1 : operand_words(levels); }
 int64_t obg_build_workspace_bytes(int n_trees, int n_regions, int levels) {
   if (levels < 1 || levels > 8 || n_trees < 0 || n_regions < 1) return -1;
-  return int64_t(n_trees) * n_regions * cube_words(levels) * 4;
+  return int64_t(n_trees) * n_regions * ws_words(levels) * 4;
 }
 
 int obg_pack_codes(const uint8_t* pixels, int64_t n_pixels, int levels, uint32_t* codes, void* stream) {
@@ -1337,7 +1654,7 @@ int obg_pack_codes(const uint8_t* pixels, int64_t n_pixels, int levels, uint32_t
 template <int L>
 static int launch_build_flat(const uint8_t* frames, int64_t units_per_frame, int64_t total_units, int group_size,
                              uint32_t* ws, uint32_t* out_pyr, int64_t n_trees, uint32_t* zero_cube, int64_t zero_words,
-                             uint32_t* counts, cudaStream_t st) {
+                             uint32_t* counts, cudaStream_t st, int levels_out) {
   constexpr bool SMEM = L <= 6;
   const size_t smem = SMEM ? size_t(Smem<L>::alloc_words) * 4 : 0;
   // one-time per instantiation: opt in to > 48 KB dynamic smem, cache occupancy
@@ -1362,10 +1679,10 @@ static int launch_build_flat(const uint8_t* frames, int64_t units_per_frame, int
   const int grid = int((total_units + per_cta - 1) / per_cta);
   if (counts)
     k_build_flat<L, SMEM, true><<<grid, BUILD_BLOCK, smem, st>>>(frames, units_per_frame, total_units, group_size,
-                                                                 per_cta, ws, out_pyr, n_trees, zero_cube, zero_words, counts);
+                                                                 per_cta, ws, out_pyr, n_trees, zero_cube, zero_words, counts, levels_out);
   else
     k_build_flat<L, SMEM, false><<<grid, BUILD_BLOCK, smem, st>>>(frames, units_per_frame, total_units, group_size,
-                                                                  per_cta, ws, out_pyr, n_trees, zero_cube, zero_words, nullptr);
+                                                                  per_cta, ws, out_pyr, n_trees, zero_cube, zero_words, nullptr, levels_out);
   LAUNCH_CHECK("k_build_flat");
   return OBG_OK;
 }
@@ -1384,11 +1701,15 @@ static int launch_pyramid(const uint32_t* src, int64_t src_stride, bool from_cub
 
 static int merge_common(const uint32_t* pyramids, int n_trees, int n_regions, int levels, int64_t k_min,
                         uint32_t* counts, uint32_t* out, uint32_t* out_cube, int flags, void* stream);
+static int finish_operand(uint32_t* operand, int64_t n_regions, int levels, cudaStream_t st);
 
+// cube_levels: obg_build_model's flow -- K1, then k_levels_cube (cube-order
+// levels below the leaves into out_pyramids; leaves stay in the workspace)
+// instead of k_pyramid.
 static int build_presence_impl(const uint8_t* frames, int n_frames, int height, int width, int levels, int grid_rows,
                                int grid_cols, int group_size, uint32_t* out_pyramids, uint32_t* out_counts,
                                void* workspace, int64_t workspace_bytes, int flags, uint32_t* zero_cube,
-                               int64_t zero_words, void* stream) {
+                               int64_t zero_words, void* stream, bool cube_levels = false) {
   if (levels < 1 || levels > 8) return set_err(OBG_EINVAL, "levels must be in 1..8, got %d", levels);
   if (n_frames < 1) return set_err(OBG_EINVAL, "no frames given");
   if (height < 1 || width < 1) return set_err(OBG_EINVAL, "frame dimensions must be >= 1");
@@ -1410,36 +1731,47 @@ static int build_presence_impl(const uint8_t* frames, int n_frames, int height, 
   const int64_t P = int64_t(height) * width;
   const int64_t used_pixels = int64_t(n_groups) * group_size * P;
   const bool flat = n_regions == 1 && (P % 16) == 0 && (reinterpret_cast<uintptr_t>(frames) % 16) == 0;
+  // trees whose leading pyramid words K1 clears for k_pyramid's atomics
+  const int64_t clear_trees = cube_levels ? 0 : n_trees;
+  // flat L <= 6: K1 writes the cube-order upper levels itself (k_build_flat flush)
+  const int smem_levels = (cube_levels && flat && levels <= 6) ? 1 : 0;
   // The workspace is handed back all-zero by k_pyramid; a caller that keeps
   // it (OBG_WS_ZEROED) skips the clear.  Output pyramids need no memset: every
   // word is either stored once or (leading shared words) cleared by K1.
-  if (!(flags & OBG_WS_ZEROED)) CUDA_TRY(cudaMemsetAsync(ws, 0, size_t(n_trees * CW * 4), st));
+  if (!(flags & OBG_WS_ZEROED)) CUDA_TRY(cudaMemsetAsync(ws, 0, size_t(n_trees * ws_words(levels) * 4), st));
   if (out_counts) CUDA_TRY(cudaMemsetAsync(out_counts, 0, size_t(n_trees) * (size_t(1) << (3 * levels)) * 4, st));
   int rc = OBG_OK;
   if (flat) {
     const int64_t upf = P / 16, total_units = used_pixels / 16;
     switch (levels) {
-      case 1: rc = launch_build_flat<1>(frames, upf, total_units, group_size, ws, out_pyramids, n_trees, zero_cube, zero_words, out_counts, st); break;
-      case 2: rc = launch_build_flat<2>(frames, upf, total_units, group_size, ws, out_pyramids, n_trees, zero_cube, zero_words, out_counts, st); break;
-      case 3: rc = launch_build_flat<3>(frames, upf, total_units, group_size, ws, out_pyramids, n_trees, zero_cube, zero_words, out_counts, st); break;
-      case 4: rc = launch_build_flat<4>(frames, upf, total_units, group_size, ws, out_pyramids, n_trees, zero_cube, zero_words, out_counts, st); break;
-      case 5: rc = launch_build_flat<5>(frames, upf, total_units, group_size, ws, out_pyramids, n_trees, zero_cube, zero_words, out_counts, st); break;
-      case 6: rc = launch_build_flat<6>(frames, upf, total_units, group_size, ws, out_pyramids, n_trees, zero_cube, zero_words, out_counts, st); break;
-      case 7: rc = launch_build_flat<7>(frames, upf, total_units, group_size, ws, out_pyramids, n_trees, zero_cube, zero_words, out_counts, st); break;
-      default: rc = launch_build_flat<8>(frames, upf, total_units, group_size, ws, out_pyramids, n_trees, zero_cube, zero_words, out_counts, st); break;
+      case 1: rc = launch_build_flat<1>(frames, upf, total_units, group_size, ws, out_pyramids, clear_trees, zero_cube, zero_words, out_counts, st, smem_levels); break;
+      case 2: rc = launch_build_flat<2>(frames, upf, total_units, group_size, ws, out_pyramids, clear_trees, zero_cube, zero_words, out_counts, st, smem_levels); break;
+      case 3: rc = launch_build_flat<3>(frames, upf, total_units, group_size, ws, out_pyramids, clear_trees, zero_cube, zero_words, out_counts, st, smem_levels); break;
+      case 4: rc = launch_build_flat<4>(frames, upf, total_units, group_size, ws, out_pyramids, clear_trees, zero_cube, zero_words, out_counts, st, smem_levels); break;
+      case 5: rc = launch_build_flat<5>(frames, upf, total_units, group_size, ws, out_pyramids, clear_trees, zero_cube, zero_words, out_counts, st, smem_levels); break;
+      case 6: rc = launch_build_flat<6>(frames, upf, total_units, group_size, ws, out_pyramids, clear_trees, zero_cube, zero_words, out_counts, st, smem_levels); break;
+      case 7: rc = launch_build_flat<7>(frames, upf, total_units, group_size, ws, out_pyramids, clear_trees, zero_cube, zero_words, out_counts, st, smem_levels); break;
+      default: rc = launch_build_flat<8>(frames, upf, total_units, group_size, ws, out_pyramids, clear_trees, zero_cube, zero_words, out_counts, st, smem_levels); break;
     }
   } else {
     const int grid = grid_for(used_pixels, 256, sm_count() * 8);
     if (out_counts)
       k_build_generic<true><<<grid, 256, 0, st>>>(frames, used_pixels, height, width, levels, grid_rows, grid_cols,
-                                                   group_size, ws, out_pyramids, n_trees, zero_cube, zero_words, out_counts);
+                                                   group_size, ws, out_pyramids, clear_trees, zero_cube, zero_words, out_counts);
     else
       k_build_generic<false><<<grid, 256, 0, st>>>(frames, used_pixels, height, width, levels, grid_rows, grid_cols,
-                                                    group_size, ws, out_pyramids, n_trees, zero_cube, zero_words, nullptr);
+                                                    group_size, ws, out_pyramids, clear_trees, zero_cube, zero_words, nullptr);
     LAUNCH_CHECK("k_build_generic");
   }
   if (rc != OBG_OK) return rc;
-  return launch_pyramid(ws, CW, true, n_trees, levels, out_pyramids, st);
+  if (cube_levels) {
+    if (levels > 1 && !smem_levels) {
+      k_levels_cube<<<unsigned(n_trees), LVL_BLOCK, 0, st>>>(ws, levels);
+      LAUNCH_CHECK("k_levels_cube");
+    }
+    return OBG_OK;
+  }
+  return launch_pyramid(ws, ws_words(levels), true, n_trees, levels, out_pyramids, st);
 }
 
 int obg_build_presence(const uint8_t* frames, int n_frames, int height, int width, int levels, int grid_rows,
@@ -1457,14 +1789,25 @@ int obg_build_model(const uint8_t* frames, int n_frames, int height, int width, 
   if (k_min < 1) return set_err(OBG_EINVAL, "k_min must be >= 1, got %lld", (long long)k_min);
   if (!out_merged || !out_cube) return set_err(OBG_EINVAL, "null buffer");
   if (levels < 1 || levels > 8) return set_err(OBG_EINVAL, "levels must be in 1..8, got %d", levels);
+  if (!tree_pyramids) return set_err(OBG_EINVAL, "null buffer");
   const int64_t n_regions = int64_t(grid_rows) * grid_cols;
-  // the build kernel clears the cube the merge scatters into: no memsets at all
+  // K1 + K2c (cube-order levels), K3c (merge; stores every operand word and
+  // zeroes the workspace), K4 (path-order merged pyramid): no memsets at all
   int rc = build_presence_impl(frames, n_frames, height, width, levels, grid_rows, grid_cols, group_size,
-                               tree_pyramids, nullptr, workspace, workspace_bytes, flags, out_cube,
-                               n_regions * operand_words(levels), stream);
+                               tree_pyramids, nullptr, workspace, workspace_bytes, flags, nullptr, 0, stream,
+                               /*cube_levels=*/true);
   if (rc != OBG_OK) return rc;
-  return merge_common(tree_pyramids, n_frames / group_size, int(n_regions), levels, k_min, nullptr, out_merged,
-                      out_cube, OBG_CUBE_ZEROED, stream);
+  cudaStream_t st = as_stream(stream);
+  const int n_groups = n_frames / group_size;
+  const int64_t words = pyr_words(levels) * n_regions;
+  if (n_regions > 65535) return set_err(OBG_EUNSUPPORTED, "too many regions (%lld > 65535)", (long long)n_regions);
+  k_merge_cube<<<dim3(unsigned((pyr_words(levels) + 31) / 32), unsigned(n_regions)), dim3(32, MERGE_GROUPS_C), 0, st>>>(
+      tree_pyramids, static_cast<uint32_t*>(workspace), n_groups, int(n_regions), levels, k_min, out_cube);
+  LAUNCH_CHECK("k_merge_cube");
+  k_morton_merged<<<grid_for(words, 256, sm_count() * 8), 256, 0, st>>>(tree_pyramids, out_cube, int(n_regions),
+                                                                         levels, out_merged);
+  LAUNCH_CHECK("k_morton_merged");
+  return finish_operand(out_cube, n_regions, levels, st);
 }
 
 int obg_pyramid_from_leaves(const uint32_t* leaves, int n_trees, int levels, uint32_t* out_pyramids, void* stream) {

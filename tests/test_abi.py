@@ -39,7 +39,7 @@ def test_size_helpers():
         for l in range(1, L + 1):
             assert lib.obg_level_offset(L, l) == _lib.level_offset(l)
     assert lib.obg_pyramid_words(0) == -1 and lib.obg_pyramid_words(9) == -1
-    assert lib.obg_build_workspace_bytes(64, 1, 6) == 64 * 8192 * 4
+    assert lib.obg_build_workspace_bytes(64, 1, 6) == 64 * (8192 + 1184) * 4   # leaf cube + upper levels (padded)
 
 
 @pytest.mark.parametrize("call", [
