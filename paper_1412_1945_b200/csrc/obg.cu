@@ -616,12 +616,21 @@ __device__ __forceinline__ void build_unit(const uint32_t (&w)[12], uint32_t* bi
       // warp-uniform skip; otherwise every lane issues four atomics, those
       // of pixels that did not miss aimed at the lane's private dummy word:
       // no per-lane branches or convergence barriers around the rare path
+      // Which of the four lookups missed in some lane (one REDUX): only
+      // those issue atomics -- a slow group usually has one miss among 128
+      // pixels, and shared atomics are the costliest MIO traffic (ncu r16:
+      // the MIO queue, not memory latency, throttles this kernel).
       const bool miss = valid && !(v[0] & v[1] & v[2] & v[3] & 1u);
       if (__any_sync(0xFFFFFFFFu, miss)) {
+        const uint32_t mm = valid ? ((~v[0] & 1u) | ((~v[1] & 1u) << 1) | ((~v[2] & 1u) << 2) | ((~v[3] & 1u) << 3))
+                                  : 0u;
+        const uint32_t rm = __reduce_or_sync(0xFFFFFFFFu, mm);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const uint32_t o = (valid && !(v[j] & 1u)) ? addr[j] : dummy;
-          reds_or_at(o, Smem<L>::set_mask(bsel[j]));
+          if (rm & (1u << j)) {
+            const uint32_t o = (mm & (1u << j)) ? addr[j] : dummy;
+            reds_or_at(o, Smem<L>::set_mask(bsel[j]));
+          }
         }
       }
     } else {
@@ -639,6 +648,53 @@ __device__ __forceinline__ void build_unit(const uint32_t (&w)[12], uint32_t* bi
       for (int j = 0; j < 16; ++j) count_code<L>(cnt, operand_to_cube<L>(px[j]));
     }
   }
+}
+
+// End of a tree segment: OR the CTA's non-zero bitset words into the tree's
+// workspace cube `dst` and, for obg_build_model (levels_out), its cube-order
+// levels L-1..1 into the tree's upper levels at dst + CW (OR of partial
+// presence = presence of the union, so the segments of one tree combine
+// with atomics).  Cube-order levels are a few instructions per word;
+// path-order ones here cost 5.5x K1's flush (ncu r8), which is why those
+// are made once, for the merged model.  Leaves the bitset zeroed.
+template <int L, int NT>
+__device__ __forceinline__ void flush_segment(uint32_t* s_bits, uint32_t* dst, int levels_out) {
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < Smem<L>::compact; i += NT) {
+    const uint32_t p = Smem<L>::compact_word(i);
+    const uint32_t x = s_bits[p];
+    if (x) flush_smem_word<L>(dst, p, x);
+  }
+  if constexpr (L >= 2) {
+    if (levels_out) {
+      uint32_t* up = dst + cube_words(L);
+      uint32_t* sc = s_bits + Smem<L>::SCRATCH;
+      constexpr uint32_t NW = uint32_t(level_words(L - 1));
+      constexpr uint32_t OFF = uint32_t(level_offset(L - 1));
+      for (uint32_t pw = threadIdx.x; pw < NW; pw += NT) {
+        const uint32_t v = level_below_from_smem<L>(s_bits, pw);
+        sc[OFF + pw] = v;
+        if (v) atomicOr(up + OFF + pw, v);
+      }
+      __syncthreads();
+      for (int l = L - 2; l >= 1; --l) {
+        const uint32_t nw = uint32_t(level_words(l)), off = uint32_t(level_offset(l));
+        const uint32_t* child = sc + level_offset(l + 1);
+        for (uint32_t pw = threadIdx.x; pw < nw; pw += NT) {
+          const uint32_t v = reduce_cube_word(child, l, pw);
+          sc[off + pw] = v;
+          if (v) atomicOr(up + off + pw, v);
+        }
+        __syncthreads();
+      }
+    } else {
+      __syncthreads();
+    }
+  } else {
+    __syncthreads();
+  }
+  for (uint32_t i = threadIdx.x; i < Smem<L>::compact; i += NT) s_bits[Smem<L>::compact_word(i)] = 0u;
+  __syncthreads();
 }
 
 template <int L, bool SMEM_BITS, bool COUNTS>
@@ -683,19 +739,6 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
     int64_t wv = u + threadIdx.x - lane;
     uint32_t wa[12], wb[12];
     if (wv + lane < seg_end) load_unit(frames, wv + lane, wa);
-#if defined(OBG_EXP) && OBG_EXP == 1
-    // experiment: lookups only (no frame traffic after the first unit)
-    for (; wv < seg_end; wv += BUILD_BLOCK) build_unit<L, SMEM_BITS, COUNTS, true>(wa, bits, cnt, true, dummy);
-#elif defined(OBG_EXP) && OBG_EXP == 2
-    // experiment: frame traffic only
-    uint32_t acc = 0;
-    for (; wv < seg_end; wv += BUILD_BLOCK) {
-      if (wv + lane < seg_end) load_unit(frames, wv + lane, wb);
-#pragma unroll
-      for (int i = 0; i < 12; ++i) acc ^= wb[i];
-    }
-    if (acc == 0x12345678u) s_bits[0] = acc;
-#endif
     while (wv < seg_end) {
       {
         const int64_t wn = wv + BUILD_BLOCK;
@@ -713,51 +756,7 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
         wv = wn;
       }
     }
-    if constexpr (SMEM_BITS) {
-      // OR the CTA's non-zero words into the tree's cube bitset and, for
-      // obg_build_model, its cube-order levels L-1..1 into the tree's upper
-      // levels (OR of partial presence = presence of the union, so segments
-      // of one tree combine with atomics).  Cube-order levels are a few
-      // instructions per word; path-order ones here cost 5.5x K1's flush
-      // (ncu r8), which is why those are made once, for the merged model.
-      __syncthreads();
-      uint32_t* dst = ws + tree * WSW;
-      for (uint32_t i = threadIdx.x; i < Smem<L>::compact; i += BUILD_BLOCK) {
-        const uint32_t p = Smem<L>::compact_word(i);
-        const uint32_t x = s_bits[p];
-        if (x) flush_smem_word<L>(dst, p, x);
-      }
-      if constexpr (L >= 2) {
-        if (levels_out) {
-          uint32_t* up = dst + CW;
-          uint32_t* sc = s_bits + Smem<L>::SCRATCH;
-          constexpr uint32_t NW = uint32_t(level_words(L - 1));
-          constexpr uint32_t OFF = uint32_t(level_offset(L - 1));
-          for (uint32_t pw = threadIdx.x; pw < NW; pw += BUILD_BLOCK) {
-            const uint32_t v = level_below_from_smem<L>(s_bits, pw);
-            sc[OFF + pw] = v;
-            if (v) atomicOr(up + OFF + pw, v);
-          }
-          __syncthreads();
-          for (int l = L - 2; l >= 1; --l) {
-            const uint32_t nw = uint32_t(level_words(l)), off = uint32_t(level_offset(l));
-            const uint32_t* child = sc + level_offset(l + 1);
-            for (uint32_t pw = threadIdx.x; pw < nw; pw += BUILD_BLOCK) {
-              const uint32_t v = reduce_cube_word(child, l, pw);
-              sc[off + pw] = v;
-              if (v) atomicOr(up + off + pw, v);
-            }
-            __syncthreads();
-          }
-        } else {
-          __syncthreads();
-        }
-      } else {
-        __syncthreads();
-      }
-      for (uint32_t i = threadIdx.x; i < Smem<L>::compact; i += BUILD_BLOCK) s_bits[Smem<L>::compact_word(i)] = 0u;
-      __syncthreads();
-    }
+    if constexpr (SMEM_BITS) flush_segment<L, BUILD_BLOCK>(s_bits, ws + tree * WSW, levels_out);
     u = seg_end;
   }
 }
