@@ -408,9 +408,28 @@ def run_ours(args):
     try:   # dram read+write of the classify kernel from the committed ncu --set full capture
         with open(os.path.join(REPO, "profiles", "traffic.json")) as f:
             tj = json.load(f)
-        traffic = int(tj["dram_bytes_read"] + tj["dram_bytes_write"])
+        if tj.get("workload") == [scene.config_id, scene.width, scene.height, cfg.levels, n_test]:
+            traffic = int(tj["dram_bytes_read"] + tj["dram_bytes_write"])   # captured on this workload only
     except Exception:
         pass
+    L = cfg.levels
+    flat = (P % 16) == 0 and cfg.grid_rows * cfg.grid_cols == 1
+    # obg_build_model's kernels (include/obg.h) + obg_classify's
+    launches = {("k_build_flat" if flat else "k_build_generic"): 1}
+    if L >= 7 or not flat:
+        launches["k_levels_cube"] = 1
+    launches.update({"k_merge_cube": 1, "k_morton_merged": 1})
+    if L == 7:
+        launches["k_l7_states"] = 1
+    cls_kernel = (f"k_classify_flat<{L}>" if L <= 6 else "k_classify_l7" if L == 7 else "k_classify_flat<8>")
+    if not flat:
+        cls_kernel = "k_classify_generic"
+    launches[cls_kernel] = 1
+    if world > 1:   # sharded build (distributed.py): presence + counts, all-reduce, threshold
+        launches = {("k_build_flat" if flat else "k_build_generic"): 1, "k_pyramid": 1, "k_merge(counts)": 1,
+                    "k_threshold": 1, cls_kernel: 1}
+        if L == 7:
+            launches["k_l7_states"] = 1
     cls_bytes = n_test * P * 4                 # 3 B read + 1 B mask written per pixel
     build_bytes = n_train * (P * 3 + obg._lib.cube_words(cfg.levels) * 4)
     cls_gbs = cls_bytes / (cls_avg / 1000) / 1e9
@@ -425,8 +444,8 @@ def run_ours(args):
             "metric": METRIC, "value": round(value, 3), "unit": "Mpx/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-            "data": "synthetic (seeded scenes with BASELINE config 3 shapes: gradient + N(0,3) noise, 20% "
-                    "bimodal swaying rows, 10% bootstrapped training frames, 8 moving ellipses)",
+            "data": f"synthetic (seeded scene generator for BASELINE config {scene.config_id}: its frame shape, "
+                    "depth, threshold and background/foreground distributions; paper_1412_1945_b200/scenes.py)",
             "config": {"workload": workload_name(scene, n_train, n_test) + " (per rank)",
                        "frames_per_step": n_train + n_test, "pixels_per_step": px_step * world,
                        "parallelism": f"dp{world}" + (" (NCCL all-reduce of merge counts)" if world > 1 else ""),
@@ -437,19 +456,17 @@ def run_ours(args):
                        "build_mpx_s": round(n_train * P / (build_avg / 1000) / 1e6, 1),
                        "classify_mpx_s": round(n_test * P / (cls_avg / 1000) / 1e6, 1),
                        "build_hbm_frac": round(build_gbs / peak, 4)},
-            "roofline": {"bound": "hbm", "kernel": "k_classify_flat<6> (obg_classify)",
+            "roofline": {"bound": "hbm", "kernel": f"{cls_kernel} (obg_classify)",
                          "achieved": round(cls_gbs, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(cls_gbs / peak, 4), "traffic": traffic, "peak_source": peak_src,
                          "traffic_source": "profiles/traffic.json (ncu --set full, bytes per launch)",
                          "algorithmic_bytes_per_launch": cls_bytes,
-                         "bytes_per_unit": "4 B/px (3 read + 1 mask byte written) x 256 x 1920x1080"},
+                         "bytes_per_unit": f"4 B/px (3 read + 1 mask byte written) x {n_test} x "
+                                           f"{scene.width}x{scene.height}"},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": args.steps * (5 if world > 1 else 4),
-            "gpu_launches_per_step": ({"k_build_flat": 1, "k_pyramid": 1, "k_merge": 1, "k_classify_flat": 1}
-                                      if world == 1 else
-                                      {"k_build_flat": 1, "k_pyramid": 1, "k_merge(counts)": 1, "k_threshold": 1,
-                                       "k_classify_flat": 1}),
+            "gpu_launches": args.steps * sum(launches.values()),
+            "gpu_launches_per_step": launches,
             "clocks": clk,
             "parity": parity,
             "gpu": torch.cuda.get_device_name(dev),
