@@ -377,8 +377,11 @@ def test_build_model_abi_and_workspace_contract(cuda):
     from paper_1412_1945_b200.model import _WORKSPACES
     lib = _lib.load()
     rng = np.random.default_rng(77)
+    # every build flavour: flat shared-bitset K1 (L <= 6, levels at its flush),
+    # global-bitset K1 + k_levels_cube (L >= 7, generic grids / odd sizes)
     for levels, (h, w), grid in [(6, (48, 64), (1, 1)), (5, (33, 20), (2, 3)), (7, (32, 32), (1, 1)),
-                                 (3, (16, 16), (1, 1))]:
+                                 (3, (16, 16), (1, 1)), (8, (16, 16), (1, 1)), (1, (16, 16), (1, 1)),
+                                 (2, (20, 12), (2, 2)), (4, (64, 32), (1, 1)), (6, (9, 13), (1, 1))]:
         base = rng.integers(0, 256, size=(1, 1, 1, 3))
         frames = np.clip(base + rng.integers(-30, 31, size=(10, h, w, 3)), 0, 255).astype(np.uint8)
         dev = cuda.from_numpy(frames).cuda()
@@ -394,3 +397,20 @@ def test_build_model_abi_and_workspace_contract(cuda):
         cuda.cuda.synchronize()
         for ws in _WORKSPACES.values():
             assert int(ws.count_nonzero()) == 0
+
+
+@pytest.mark.gpu
+def test_build_model_groups_and_repeat(cuda):
+    """Groups of frames per tree (segments of a CTA end mid-range), a dropped
+    trailing partial group, and back-to-back builds reusing the kept
+    workspace (zero-on-return)."""
+    rng = np.random.default_rng(5)
+    for levels, gs in [(6, 3), (5, 2), (7, 4)]:
+        frames = rng.integers(0, 256, size=(11, 40, 64, 3), dtype=np.uint8)
+        frames[:, :20] = frames[0, :20]                      # half of each frame static
+        dev = cuda.from_numpy(frames).cuda()
+        cfg = ModelConfig(levels=levels, threshold=0.5, group_size=gs, training_frames=11)
+        want = orc.build_background_model(list(frames), levels, 0.5, group_size=gs)
+        for _ in range(3):
+            model = obg.build_background_model_device(dev, cfg)
+            assert model.trees[0][0].to_bytes() == orc.to_bytes(want[(0, 0)])
