@@ -415,7 +415,7 @@ def run_ours(args):
     L = cfg.levels
     flat = (P % 16) == 0 and cfg.grid_rows * cfg.grid_cols == 1
     # obg_build_model's kernels (include/obg.h) + obg_classify's
-    launches = {("k_build_flat" if flat else "k_build_generic"): 1}
+    launches = {("k_build_generic" if not flat else "k_build_l7h" if L == 7 else "k_build_flat"): 1}
     if L >= 7 or not flat:
         launches["k_levels_cube"] = 1
     launches.update({"k_merge_cube": 1, "k_morton_merged": 1})

@@ -761,6 +761,119 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
   }
 }
 
+// ---------------------------------------------------------------------------
+// K1, L = 7: the 2^21-bit leaf set (256 KB) does not fit shared memory, so
+// the CTA streams its range twice, once per half of the cube (R' top bit h),
+// with that half (128 KB, skewed rows: R' & 63 x 128 G' x 4 B' words + pad)
+// in shared memory; pixels of the other half count as hits.  Two frame reads
+// instead of a global check-before-set per pixel: on uniform-random frames
+// (~2 M distinct leaves per frame) the global bitset path made every lookup
+// an L2 round trip and every first sight of a leaf a global atomic (r1:
+// 0.07 of HBM).  1024 threads, one CTA per SM.
+// ---------------------------------------------------------------------------
+constexpr int L7H_BLOCK = 1024;
+constexpr uint32_t L7H_ROWW = 512 + 5;                 // words per R' row (128 G' x 4) + pad
+constexpr uint32_t L7H_WORDS = 64 * L7H_ROWW;          // one half of the cube
+constexpr uint32_t L7H_ALLOC = L7H_WORDS + 32;         // + per-lane dummy words
+
+// x = [*, G, B, R]: byte offset in the half-cube, bit selector, half of R'
+__device__ __forceinline__ void l7h_position(uint32_t x, uint32_t& off, uint32_t& bsel, uint32_t& half) {
+  const uint32_t r6 = __umulhi(x, 1u << 7) & 63u;                          // (x >> 25) & 63
+  const uint32_t g = __umulhi(x, 1u << 27) & 0x7F0u;                       // G' << 4
+  const uint32_t b = __umulhi(x, 1u << 12) & 0xCu;                         // (B' >> 5) << 2
+  off = r6 * (L7H_ROWW * 4u) + (g | b);
+  bsel = __umulhi(x, 1u << 15);                                           // x >> 17: B' in the low bits
+  half = x >> 31;
+}
+
+__device__ __forceinline__ void build_unit_l7h(const uint32_t (&w)[12], uint32_t hpass, bool valid, uint32_t dummy) {
+  uint32_t px[16];
+  unpack16<0, 6>(w, px);                                                  // [*, G, B, R] operands
+#pragma unroll
+  for (int g = 0; g < 16; g += 4) {
+    uint32_t addr[4], bsel[4], v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint32_t half;
+      l7h_position(px[g + j], addr[j], bsel[j], half);
+      const uint32_t wd = lds_at(addr[j]);
+      v[j] = __funnelshift_r(wd, wd, bsel[j]) | (half ^ hpass);            // other half: a hit
+    }
+    const bool miss = valid && !(v[0] & v[1] & v[2] & v[3] & 1u);
+    if (__any_sync(0xFFFFFFFFu, miss)) {
+      const uint32_t mm = valid ? ((~v[0] & 1u) | ((~v[1] & 1u) << 1) | ((~v[2] & 1u) << 2) | ((~v[3] & 1u) << 3))
+                                : 0u;
+      const uint32_t rm = __reduce_or_sync(0xFFFFFFFFu, mm);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (rm & (1u << j)) {
+          const uint32_t o = (mm & (1u << j)) ? addr[j] : dummy;
+          reds_or_at(o, 1u << (bsel[j] & 31u));
+        }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(L7H_BLOCK, 1)
+k_build_l7h(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t total_units, int group_size,
+            int64_t units_per_cta, uint32_t* __restrict__ ws, uint32_t* __restrict__ out_pyr, int64_t n_trees,
+            uint32_t* __restrict__ zero_cube, int64_t zero_words) {
+  extern __shared__ __align__(1024) uint32_t s_bits[];
+  if (static_cast<uint32_t>(__cvta_generic_to_shared(s_bits)) != DYN_SMEM_BASE) __trap();
+  constexpr int64_t WSW = ws_words(7);
+  if (blockIdx.x == 0) {
+    clear_shared_words(out_pyr, n_trees, 7);
+    for (int64_t i = threadIdx.x; i < zero_words; i += L7H_BLOCK) zero_cube[i] = 0u;
+  }
+  const int64_t u_begin = int64_t(blockIdx.x) * units_per_cta;
+  const int64_t u_end = min(total_units, u_begin + units_per_cta);
+  if (u_begin >= u_end) return;
+  for (uint32_t i = threadIdx.x; i < L7H_WORDS; i += L7H_BLOCK) s_bits[i] = 0u;
+  __syncthreads();
+  const int64_t upt = units_per_frame * group_size;
+  const int lane = threadIdx.x & 31;
+  const uint32_t dummy = 4u * (L7H_WORDS + uint32_t(lane));
+  for (uint32_t h = 0; h < 2; ++h) {
+    int64_t u = u_begin;
+    while (u < u_end) {
+      const int64_t tree = u / upt;
+      const int64_t seg_end = min(u_end, (tree + 1) * upt);
+      int64_t wv = u + threadIdx.x - lane;
+      uint32_t wa[12], wb[12];
+      if (wv + lane < seg_end) load_unit(frames, wv + lane, wa);
+      while (wv < seg_end) {
+        {
+          const int64_t wn = wv + L7H_BLOCK;
+          if (wn + lane < seg_end) load_unit(frames, wn + lane, wb);
+          build_unit_l7h(wa, h, wv + lane < seg_end, dummy);
+          wv = wn;
+        }
+        if (wv >= seg_end) break;
+        {
+          const int64_t wn = wv + L7H_BLOCK;
+          if (wn + lane < seg_end) load_unit(frames, wn + lane, wa);
+          build_unit_l7h(wb, h, wv + lane < seg_end, dummy);
+          wv = wn;
+        }
+      }
+      // flush this half of the tree's leaf cube, leave the half-cube zeroed
+      __syncthreads();
+      uint32_t* dst = ws + tree * WSW;
+      for (uint32_t p = threadIdx.x; p < L7H_WORDS; p += L7H_BLOCK) {
+        const uint32_t x = s_bits[p];
+        if (x) {
+          const uint32_t r6 = p / L7H_ROWW, c = p - r6 * L7H_ROWW;          // c < 512: pads stay 0
+          atomicOr(dst + (((64u * h + r6) << 9) | c), x);
+          s_bits[p] = 0u;
+        }
+      }
+      __syncthreads();
+      u = seg_end;
+    }
+  }
+}
+
 // Generic path: any grid, any frame size / alignment.  One thread per pixel,
 // region via region_of (model.py:61-66), bits in the workspace (global).
 template <bool COUNTS>
@@ -1686,6 +1799,26 @@ static int launch_build_flat(const uint8_t* frames, int64_t units_per_frame, int
   return OBG_OK;
 }
 
+static int launch_build_l7h(const uint8_t* frames, int64_t units_per_frame, int64_t total_units, int group_size,
+                            uint32_t* ws, uint32_t* out_pyr, int64_t n_trees, uint32_t* zero_cube, int64_t zero_words,
+                            cudaStream_t st) {
+  constexpr size_t smem = size_t(L7H_ALLOC) * 4;
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(k_build_l7h, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
+  const int64_t max_ctas = sm_count();                   // one CTA per SM
+  int64_t per_cta = (total_units + max_ctas - 1) / max_ctas;
+  const int64_t min_per_cta = int64_t(L7H_BLOCK) * 4;
+  if (per_cta < min_per_cta) per_cta = min_per_cta;
+  const int grid = int((total_units + per_cta - 1) / per_cta);
+  k_build_l7h<<<grid, L7H_BLOCK, smem, st>>>(frames, units_per_frame, total_units, group_size, per_cta, ws, out_pyr,
+                                             n_trees, zero_cube, zero_words);
+  LAUNCH_CHECK("k_build_l7h");
+  return OBG_OK;
+}
+
 static int launch_pyramid(const uint32_t* src, int64_t src_stride, bool from_cube, int64_t n_trees, int L,
                           uint32_t* out, cudaStream_t st) {
   const int64_t LW = level_words(L);
@@ -1749,7 +1882,12 @@ static int build_presence_impl(const uint8_t* frames, int n_frames, int height, 
       case 4: rc = launch_build_flat<4>(frames, upf, total_units, group_size, ws, out_pyramids, clear_trees, zero_cube, zero_words, out_counts, st, smem_levels); break;
       case 5: rc = launch_build_flat<5>(frames, upf, total_units, group_size, ws, out_pyramids, clear_trees, zero_cube, zero_words, out_counts, st, smem_levels); break;
       case 6: rc = launch_build_flat<6>(frames, upf, total_units, group_size, ws, out_pyramids, clear_trees, zero_cube, zero_words, out_counts, st, smem_levels); break;
-      case 7: rc = launch_build_flat<7>(frames, upf, total_units, group_size, ws, out_pyramids, clear_trees, zero_cube, zero_words, out_counts, st, smem_levels); break;
+      case 7:
+        rc = out_counts ? launch_build_flat<7>(frames, upf, total_units, group_size, ws, out_pyramids, clear_trees,
+                                               zero_cube, zero_words, out_counts, st, smem_levels)
+                        : launch_build_l7h(frames, upf, total_units, group_size, ws, out_pyramids, clear_trees,
+                                           zero_cube, zero_words, st);
+        break;
       default: rc = launch_build_flat<8>(frames, upf, total_units, group_size, ws, out_pyramids, clear_trees, zero_cube, zero_words, out_counts, st, smem_levels); break;
     }
   } else {
