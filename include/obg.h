@@ -141,6 +141,19 @@ int obg_classify(const uint8_t* frames, int n_frames, int height, int width, int
                  int grid_rows, int grid_cols, const uint32_t* cube_bits,
                  uint8_t* mask, int mask_format, void* stream);
 
+/* Classification fused with evaluation: the confusion counts of the
+ * predicted foreground against a ground-truth mask, no mask written.
+ * Replaces detect_octree followed by evaluation.accumulate
+ * (evaluation.py:38-53; foreground is the positive class).
+ *   truth  : same layout as obg_classify's mask (truth_format OBG_MASK_U8:
+ *            any nonzero byte = foreground, e.g. 0/1 or 0/255 PGM values;
+ *            OBG_MASK_PACKED: bit-packed).
+ *   counts : device u64 [4] = tn, tp, fn, fp, ADDED to (like accumulate's
+ *            stats argument). */
+int obg_classify_confusion(const uint8_t* frames, int n_frames, int height, int width, int levels,
+                           int grid_rows, int grid_cols, const uint32_t* cube_bits,
+                           const uint8_t* truth, int truth_format, uint64_t* counts, void* stream);
+
 /* Preorder child-mask serialization of one pyramid (Octree.to_bytes,
  * octree.py:217-227, 258-267) computed on the device.
  *   has_root : 1 if the tree has a root node.

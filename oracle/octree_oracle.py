@@ -204,3 +204,14 @@ def prune(tree: OracleTree, new_depth: int) -> OracleTree:
     out = OracleTree(new_depth, root=tree.root)
     out.levels = {l: tree.level(l) for l in range(1, new_depth + 1)} if tree.root else {}
     return out
+
+
+# --- evaluation.py:38-53 (accumulate): confusion counts, foreground positive ----------
+def confusion(predicted, truth) -> tuple:
+    """(tn, tp, fn, fp) of one predicted / truth mask pair (evaluation.py:38-53)."""
+    p = np.asarray(predicted, dtype=bool)
+    t = np.asarray(truth, dtype=bool)
+    if p.shape != t.shape:
+        raise ValueError(f"mask dimensions {p.shape} vs {t.shape} do not match")
+    return (int(np.count_nonzero(~p & ~t)), int(np.count_nonzero(p & t)),
+            int(np.count_nonzero(~p & t)), int(np.count_nonzero(p & ~t)))

@@ -45,10 +45,11 @@ SIGNATURES = {
     "obg_merge": (_I, [_P, _I, _I, _I, _L, _P, _P, _P]),
     "obg_leaf_cube": (_I, [_P, _I, _I, _P, _P]),
     "obg_classify": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _P, _I, _P]),
+    "obg_classify_confusion": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _P, _I, _P, _P]),
     "obg_serialize_workspace_bytes": (_L, [_I]),
     "obg_serialize": (_I, [_P, _I, _I, _P, _L, ctypes.POINTER(ctypes.c_int64), _P, _L, _P]),
 }
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 
 class LibraryNotBuilt(RuntimeError):

@@ -24,7 +24,7 @@
 
 #include "../../include/obg.h"
 
-#define OBG_ABI_VERSION 2
+#define OBG_ABI_VERSION 3
 #define OBG_CUBE_ZEROED 0x100   /* internal: out_cube already cleared by the build kernel */
 
 // ---------------------------------------------------------------------------
@@ -1432,6 +1432,28 @@ constexpr int CLS_BLOCK = 256;
 // Flat path: 1x1 grid, leaf cube bitset in shared memory (L <= 6) or read
 // through L1/L2 (L >= 7).  One thread = one 16-pixel unit per iteration:
 // 3 x 16-byte loads, 16 lookups, one 16-byte (u8) or 2-byte (packed) store.
+
+// What the classify kernels do with a unit's 16 presence bits: write the
+// foreground mask (u8 or bit-packed), or -- fused evaluation, SURVEY.md
+// §8(f) row 3 / evaluation.py:38-53 -- compare with a ground-truth mask and
+// count the confusion (tn, tp, fn, fp) without writing any mask.
+enum { OUT_U8 = 0, OUT_PACKED = 1, OUT_CONF_U8 = 2, OUT_CONF_PACKED = 3 };
+struct ConfAcc {
+  uint32_t tn = 0, tp = 0, fn = 0, fp = 0;
+  __device__ __forceinline__ void add(uint32_t fg, uint32_t t, uint32_t valid) {
+    tp += __popc(fg & t & valid);
+    fp += __popc(fg & ~t & valid);
+    fn += __popc(~fg & t & valid);
+    tn += __popc(~fg & ~t & valid);
+  }
+};
+
+// nonzero bytes of x -> bits 0..3
+__device__ __forceinline__ uint32_t nz_nibble(uint32_t x) {
+  const uint32_t hi = (((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u;
+  return ((hi >> 7) * 0x01020408u) >> 24;
+}
+
 // Presence bits (bit 0 of v[j]) of a 16-pixel unit -> 16 foreground mask
 // bytes (one 16-byte streaming store) or 16 mask bits.
 template <bool PACKED>
@@ -1453,10 +1475,51 @@ __device__ __forceinline__ void store_mask16(const uint32_t (&v)[16], uint8_t* m
   }
 }
 
+template <int OUT>
+__device__ __forceinline__ void emit16(const uint32_t (&v)[16], uint8_t* out, int64_t u, ConfAcc& acc) {
+  if constexpr (OUT == OUT_U8 || OUT == OUT_PACKED) {
+    store_mask16<OUT == OUT_PACKED>(v, out, u);
+  } else {
+    uint32_t bg = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) bg |= (v[j] & 1u) << j;
+    uint32_t t;
+    if constexpr (OUT == OUT_CONF_U8) {
+      const uint4 q = __ldcs(reinterpret_cast<const uint4*>(out) + u);
+      t = nz_nibble(q.x) | (nz_nibble(q.y) << 4) | (nz_nibble(q.z) << 8) | (nz_nibble(q.w) << 12);
+    } else {
+      t = __ldcs(reinterpret_cast<const uint16_t*>(out) + u);
+    }
+    acc.add(~bg, t, 0xFFFFu);
+  }
+}
+
+// single pixel i (tails): fg = 1 for foreground
+template <int OUT>
+__device__ __forceinline__ void emit1(uint32_t fg, uint8_t* out, int64_t i, ConfAcc& acc) {
+  if constexpr (OUT == OUT_U8) out[i] = uint8_t(fg);
+  else if constexpr (OUT == OUT_CONF_U8) acc.add(fg, out[i] != 0 ? 1u : 0u, 1u);
+}
+
+// block-end: warp sums, one 64-bit atomic per counter and warp
+template <int OUT>
+__device__ __forceinline__ void flush_conf(const ConfAcc& acc, unsigned long long* counts) {
+  if constexpr (OUT == OUT_CONF_U8 || OUT == OUT_CONF_PACKED) {
+    const uint32_t tn = __reduce_add_sync(0xFFFFFFFFu, acc.tn), tp = __reduce_add_sync(0xFFFFFFFFu, acc.tp);
+    const uint32_t fn = __reduce_add_sync(0xFFFFFFFFu, acc.fn), fp = __reduce_add_sync(0xFFFFFFFFu, acc.fp);
+    if ((threadIdx.x & 31) == 0) {
+      if (tn) atomicAdd(counts + 0, (unsigned long long)tn);
+      if (tp) atomicAdd(counts + 1, (unsigned long long)tp);
+      if (fn) atomicAdd(counts + 2, (unsigned long long)fn);
+      if (fp) atomicAdd(counts + 3, (unsigned long long)fp);
+    }
+  }
+}
+
 // One 16-pixel unit -> 16 mask bytes (or 16 mask bits).
-template <int L, bool SMEM_BITS, bool PACKED>
+template <int L, bool SMEM_BITS, int OUT>
 __device__ __forceinline__ void classify_unit(const uint32_t (&w)[12], const uint32_t* bits, uint8_t* mask,
-                                              int64_t u) {
+                                              int64_t u, ConfAcc& acc) {
   const char* base = reinterpret_cast<const char*>(bits);
   uint32_t v[16];
   if constexpr (SMEM_BITS) {
@@ -1481,13 +1544,16 @@ __device__ __forceinline__ void classify_unit(const uint32_t (&w)[12], const uin
       v[j] = __funnelshift_r(wd, wd, bsel);
     }
   }
-  store_mask16<PACKED>(v, mask, u);
+  emit16<OUT>(v, mask, u, acc);
 }
 
-template <int L, bool SMEM_BITS, bool PACKED>
+// `mask`: the output mask (OUT_U8 / OUT_PACKED) or the truth mask read by
+// the fused evaluation (OUT_CONF_*, counts += tn, tp, fn, fp).
+template <int L, bool SMEM_BITS, int OUT>
 __global__ void __launch_bounds__(CLS_BLOCK, 2)
 k_classify_flat(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_pixels,
-                const uint32_t* __restrict__ cube, uint8_t* __restrict__ mask) {
+                const uint32_t* __restrict__ cube, uint8_t* __restrict__ mask, unsigned long long* counts) {
+  ConfAcc acc;
   extern __shared__ uint32_t s_bits[];
   constexpr int64_t CW = cube_words(L);
   const uint32_t* bits = cube;
@@ -1506,11 +1572,11 @@ k_classify_flat(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_p
     uint32_t wa[12], wb[12];
     load_unit(frames, u, wa);
     if (second) load_unit(frames, u + stride, wb);
-    classify_unit<L, SMEM_BITS, PACKED>(wa, bits, mask, u);
-    if (second) classify_unit<L, SMEM_BITS, PACKED>(wb, bits, mask, u + stride);
+    classify_unit<L, SMEM_BITS, OUT>(wa, bits, mask, u, acc);
+    if (second) classify_unit<L, SMEM_BITS, OUT>(wb, bits, mask, u + stride, acc);
   }
-  // tail pixels (n_pixels not a multiple of 16; u8 layout only)
-  if constexpr (!PACKED) {
+  // tail pixels (n_pixels not a multiple of 16; u8 layouts only)
+  if constexpr (OUT == OUT_U8 || OUT == OUT_CONF_U8) {
     if (blockIdx.x == 0) {
       for (int64_t i = n_units * 16 + threadIdx.x; i < n_pixels; i += CLS_BLOCK) {
         const uint32_t x = Smem<L>::skew ? gbr_word_scalar(frames + 3 * i) : rgb_word_scalar(frames + 3 * i);
@@ -1518,10 +1584,11 @@ k_classify_flat(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_p
         bit_position<L, SmemC<L>>(x, addr, bsel);
         const uint32_t* wp = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(bits) + addr);
         const uint32_t wd = SMEM_BITS ? *wp : __ldg(wp);
-        mask[i] = uint8_t(((wd >> (bsel & 31u)) & 1u) ^ 1u);
+        emit1<OUT>(((wd >> (bsel & 31u)) & 1u) ^ 1u, mask, i, acc);
       }
     }
   }
+  flush_conf<OUT>(acc, counts);
 }
 
 // ---------------------------------------------------------------------------
@@ -1554,9 +1621,10 @@ __device__ __forceinline__ uint32_t l7_leaf_bit(const uint32_t* __restrict__ cub
   return (__ldg(cube + (idx >> 5)) >> (idx & 31u)) & 1u;
 }
 
-template <bool PACKED>
+template <int OUT>
 __device__ __forceinline__ void classify_unit_l7(const uint32_t (&w)[12], const uint32_t* s_state,
-                                                 const uint32_t* __restrict__ cube, uint8_t* mask, int64_t u) {
+                                                 const uint32_t* __restrict__ cube, uint8_t* mask, int64_t u,
+                                                 ConfAcc& acc) {
   uint32_t px[16], v[16];
   unpack16<0, 6>(w, px);                                            // [*, G, B, R] operands
   uint32_t mixed = 0;
@@ -1577,13 +1645,14 @@ __device__ __forceinline__ void classify_unit_l7(const uint32_t (&w)[12], const 
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] >>= 1;                        // all children present
   }
-  store_mask16<PACKED>(v, mask, u);
+  emit16<OUT>(v, mask, u, acc);
 }
 
-template <bool PACKED>
+template <int OUT>
 __global__ void __launch_bounds__(S7_BLOCK, 3)
 k_classify_l7(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_pixels, const uint32_t* __restrict__ cube,
-              uint8_t* __restrict__ mask) {
+              uint8_t* __restrict__ mask, unsigned long long* counts) {
+  ConfAcc acc;
   extern __shared__ uint32_t s_state[];
   for (uint32_t i = threadIdx.x; i < 64u * 256u; i += S7_BLOCK)       // states follow the cube (k_l7_states)
     s_state[(i >> 8) * S7_ROWW + (i & 255u)] = __ldg(cube + cube_words(7) + i);
@@ -1594,27 +1663,30 @@ k_classify_l7(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_pix
     uint32_t wa[12], wb[12];
     load_unit(frames, u, wa);
     if (second) load_unit(frames, u + stride, wb);
-    classify_unit_l7<PACKED>(wa, s_state, cube, mask, u);
-    if (second) classify_unit_l7<PACKED>(wb, s_state, cube, mask, u + stride);
+    classify_unit_l7<OUT>(wa, s_state, cube, mask, u, acc);
+    if (second) classify_unit_l7<OUT>(wb, s_state, cube, mask, u + stride, acc);
   }
-  if constexpr (!PACKED) {
+  if constexpr (OUT == OUT_U8 || OUT == OUT_CONF_U8) {
     if (blockIdx.x == 0) {
       for (int64_t i = n_units * 16 + threadIdx.x; i < n_pixels; i += S7_BLOCK) {
         const uint32_t x = gbr_word_scalar(frames + 3 * i);
         const uint32_t st = s7_state(s_state, x);
         const uint32_t bg = ((st ^ (st >> 1)) & 1u) ? l7_leaf_bit(cube, x) : (st >> 1) & 1u;
-        mask[i] = uint8_t(bg ^ 1u);
+        emit1<OUT>(bg ^ 1u, mask, i, acc);
       }
     }
   }
+  flush_conf<OUT>(acc, counts);
 }
 
 // Generic path: any grid / alignment / frame size.  One thread = 8 pixels of
 // one frame (one packed byte, or 8 u8 mask bytes).
-template <bool PACKED>
+template <int OUT>
 __global__ void __launch_bounds__(256)
 k_classify_generic(const uint8_t* __restrict__ frames, int64_t n_frames, int H, int W, int L, int R, int C,
-                   const uint32_t* __restrict__ cube, uint8_t* __restrict__ mask) {
+                   const uint32_t* __restrict__ cube, uint8_t* __restrict__ mask, unsigned long long* counts) {
+  constexpr bool PACKED = OUT == OUT_PACKED || OUT == OUT_CONF_PACKED;
+  ConfAcc acc;
   const int64_t P = int64_t(H) * W;
   const int64_t bytes_per_frame = (P + 7) / 8;
   const int64_t total = bytes_per_frame * n_frames;
@@ -1635,10 +1707,15 @@ k_classify_generic(const uint8_t* __restrict__ frames, int64_t n_frames, int H, 
       const uint32_t* bits = cube + (int64_t(row) * C + col) * operand_words(L);
       const uint32_t fg = ((__ldg(bits + (idx >> 5)) >> (idx & 31u)) & 1u) ^ 1u;
       if (PACKED) byte |= fg << k;
-      else mask[f * P + p] = uint8_t(fg);
+      else emit1<OUT>(fg, mask, f * P + p, acc);
     }
-    if (PACKED) mask[t] = uint8_t(byte);
+    if constexpr (OUT == OUT_PACKED) mask[t] = uint8_t(byte);
+    if constexpr (OUT == OUT_CONF_PACKED) {
+      const uint32_t nv = uint32_t(min(int64_t(8), P - q * 8));
+      acc.add(byte, mask[t], (1u << nv) - 1u);
+    }
   }
+  flush_conf<OUT>(acc, counts);
 }
 
 // ===========================================================================
@@ -2039,77 +2116,53 @@ int obg_leaf_cube(const uint32_t* pyramids, int n_trees, int levels, uint32_t* c
   return finish_operand(cube, n_trees, levels, as_stream(stream));
 }
 
-template <int L>
+template <int L, int OUT>
 static int launch_classify_flat(const uint8_t* frames, int64_t n_pixels, const uint32_t* cube, uint8_t* mask,
-                                bool packed, cudaStream_t st) {
+                                unsigned long long* counts, cudaStream_t st) {
   constexpr bool SMEM = L <= 6;
   const size_t smem = SMEM ? size_t(SmemC<L>::words) * 4 : 0;
   const int64_t n_units = n_pixels / 16;
-  static int occ[2] = {0, 0};
-  int& bps = occ[packed ? 1 : 0];
+  static int bps = 0;                        // per instantiation: opt in to > 48 KB smem, occupancy
   if (bps == 0) {
-    if (packed) {
-      CUDA_TRY(cudaFuncSetAttribute(k_classify_flat<L, SMEM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(smem)));
-      bps = occupancy(k_classify_flat<L, SMEM, true>, CLS_BLOCK, smem);
-    } else {
-      CUDA_TRY(cudaFuncSetAttribute(k_classify_flat<L, SMEM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(smem)));
-      bps = occupancy(k_classify_flat<L, SMEM, false>, CLS_BLOCK, smem);
-    }
+    CUDA_TRY(cudaFuncSetAttribute(k_classify_flat<L, SMEM, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(smem)));
+    bps = occupancy(k_classify_flat<L, SMEM, OUT>, CLS_BLOCK, smem);
   }
   int64_t grid = int64_t(sm_count()) * bps;
   const int64_t need = (n_units + CLS_BLOCK - 1) / CLS_BLOCK;
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
-  if (packed)
-    k_classify_flat<L, SMEM, true><<<unsigned(grid), CLS_BLOCK, smem, st>>>(frames, n_units, n_pixels, cube, mask);
-  else
-    k_classify_flat<L, SMEM, false><<<unsigned(grid), CLS_BLOCK, smem, st>>>(frames, n_units, n_pixels, cube, mask);
+  k_classify_flat<L, SMEM, OUT><<<unsigned(grid), CLS_BLOCK, smem, st>>>(frames, n_units, n_pixels, cube, mask, counts);
   LAUNCH_CHECK("k_classify_flat");
   return OBG_OK;
 }
 
+template <int OUT>
 static int launch_classify_l7(const uint8_t* frames, int64_t n_pixels, const uint32_t* cube, uint8_t* mask,
-                              bool packed, cudaStream_t st) {
+                              unsigned long long* counts, cudaStream_t st) {
   const size_t smem = size_t(S7_WORDS) * 4;
-  static int occ[2] = {0, 0};
-  int& bps = occ[packed ? 1 : 0];
+  static int bps = 0;
   if (bps == 0) {
-    if (packed) {
-      CUDA_TRY(cudaFuncSetAttribute(k_classify_l7<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      bps = occupancy(k_classify_l7<true>, S7_BLOCK, smem);
-    } else {
-      CUDA_TRY(cudaFuncSetAttribute(k_classify_l7<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      bps = occupancy(k_classify_l7<false>, S7_BLOCK, smem);
-    }
+    CUDA_TRY(cudaFuncSetAttribute(k_classify_l7<OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    bps = occupancy(k_classify_l7<OUT>, S7_BLOCK, smem);
   }
   const int64_t n_units = n_pixels / 16;
   int64_t grid = int64_t(sm_count()) * bps;
   const int64_t need = (n_units + S7_BLOCK - 1) / S7_BLOCK;
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
-  if (packed)
-    k_classify_l7<true><<<unsigned(grid), S7_BLOCK, smem, st>>>(frames, n_units, n_pixels, cube, mask);
-  else
-    k_classify_l7<false><<<unsigned(grid), S7_BLOCK, smem, st>>>(frames, n_units, n_pixels, cube, mask);
+  k_classify_l7<OUT><<<unsigned(grid), S7_BLOCK, smem, st>>>(frames, n_units, n_pixels, cube, mask, counts);
   LAUNCH_CHECK("k_classify_l7");
   return OBG_OK;
 }
 
-int obg_classify(const uint8_t* frames, int n_frames, int height, int width, int levels, int grid_rows, int grid_cols,
-                 const uint32_t* cube_bits, uint8_t* mask, int mask_format, void* stream) {
-  g_err[0] = 0;
-  if (levels < 1 || levels > 8) return set_err(OBG_EINVAL, "levels must be in 1..8, got %d", levels);
-  if (n_frames < 0) return set_err(OBG_EINVAL, "n_frames must be >= 0");
-  if (height < 1 || width < 1) return set_err(OBG_EINVAL, "frame dimensions must be >= 1");
-  if (grid_rows < 1 || grid_cols < 1) return set_err(OBG_EINVAL, "grid dimensions must be >= 1");
-  if (mask_format != OBG_MASK_U8 && mask_format != OBG_MASK_PACKED)
-    return set_err(OBG_EINVAL, "unknown mask_format %d", mask_format);
-  if (n_frames == 0) return OBG_OK;
-  if (!frames || !cube_bits || !mask) return set_err(OBG_EINVAL, "null buffer");
-  cudaStream_t st = as_stream(stream);
-  const bool packed = mask_format == OBG_MASK_PACKED;
+// obg_classify / obg_classify_confusion: `mask` is the output mask or the
+// truth mask (OUT_CONF_*), packed = bit-packed layout.
+template <int OUT>
+static int classify_dispatch(const uint8_t* frames, int n_frames, int height, int width, int levels, int grid_rows,
+                             int grid_cols, const uint32_t* cube_bits, uint8_t* mask, unsigned long long* counts,
+                             cudaStream_t st) {
+  constexpr bool packed = OUT == OUT_PACKED || OUT == OUT_CONF_PACKED;
   const int64_t P = int64_t(height) * width;
   const int64_t n_pixels = P * n_frames;
   const bool aligned = (reinterpret_cast<uintptr_t>(frames) % 16) == 0 &&
@@ -2117,26 +2170,64 @@ int obg_classify(const uint8_t* frames, int n_frames, int height, int width, int
   const bool flat = grid_rows == 1 && grid_cols == 1 && aligned && (!packed || (P % 16) == 0);
   if (flat) {
     switch (levels) {
-      case 1: return launch_classify_flat<1>(frames, n_pixels, cube_bits, mask, packed, st);
-      case 2: return launch_classify_flat<2>(frames, n_pixels, cube_bits, mask, packed, st);
-      case 3: return launch_classify_flat<3>(frames, n_pixels, cube_bits, mask, packed, st);
-      case 4: return launch_classify_flat<4>(frames, n_pixels, cube_bits, mask, packed, st);
-      case 5: return launch_classify_flat<5>(frames, n_pixels, cube_bits, mask, packed, st);
-      case 6: return launch_classify_flat<6>(frames, n_pixels, cube_bits, mask, packed, st);
-      case 7: return launch_classify_l7(frames, n_pixels, cube_bits, mask, packed, st);
-      default: return launch_classify_flat<8>(frames, n_pixels, cube_bits, mask, packed, st);
+      case 1: return launch_classify_flat<1, OUT>(frames, n_pixels, cube_bits, mask, counts, st);
+      case 2: return launch_classify_flat<2, OUT>(frames, n_pixels, cube_bits, mask, counts, st);
+      case 3: return launch_classify_flat<3, OUT>(frames, n_pixels, cube_bits, mask, counts, st);
+      case 4: return launch_classify_flat<4, OUT>(frames, n_pixels, cube_bits, mask, counts, st);
+      case 5: return launch_classify_flat<5, OUT>(frames, n_pixels, cube_bits, mask, counts, st);
+      case 6: return launch_classify_flat<6, OUT>(frames, n_pixels, cube_bits, mask, counts, st);
+      case 7: return launch_classify_l7<OUT>(frames, n_pixels, cube_bits, mask, counts, st);
+      default: return launch_classify_flat<8, OUT>(frames, n_pixels, cube_bits, mask, counts, st);
     }
   }
   const int64_t threads = ((P + 7) / 8) * n_frames;
   const int grid = grid_for(threads, 256, sm_count() * 8);
-  if (packed)
-    k_classify_generic<true><<<grid, 256, 0, st>>>(frames, n_frames, height, width, levels, grid_rows, grid_cols,
-                                                   cube_bits, mask);
-  else
-    k_classify_generic<false><<<grid, 256, 0, st>>>(frames, n_frames, height, width, levels, grid_rows, grid_cols,
-                                                    cube_bits, mask);
+  k_classify_generic<OUT><<<grid, 256, 0, st>>>(frames, n_frames, height, width, levels, grid_rows, grid_cols,
+                                                cube_bits, mask, counts);
   LAUNCH_CHECK("k_classify_generic");
   return OBG_OK;
+}
+
+static int classify_args(int n_frames, int height, int width, int levels, int grid_rows, int grid_cols,
+                         int mask_format) {
+  if (levels < 1 || levels > 8) return set_err(OBG_EINVAL, "levels must be in 1..8, got %d", levels);
+  if (n_frames < 0) return set_err(OBG_EINVAL, "n_frames must be >= 0");
+  if (height < 1 || width < 1) return set_err(OBG_EINVAL, "frame dimensions must be >= 1");
+  if (grid_rows < 1 || grid_cols < 1) return set_err(OBG_EINVAL, "grid dimensions must be >= 1");
+  if (mask_format != OBG_MASK_U8 && mask_format != OBG_MASK_PACKED)
+    return set_err(OBG_EINVAL, "unknown mask_format %d", mask_format);
+  return OBG_OK;
+}
+
+int obg_classify(const uint8_t* frames, int n_frames, int height, int width, int levels, int grid_rows, int grid_cols,
+                 const uint32_t* cube_bits, uint8_t* mask, int mask_format, void* stream) {
+  g_err[0] = 0;
+  if (int rc = classify_args(n_frames, height, width, levels, grid_rows, grid_cols, mask_format)) return rc;
+  if (n_frames == 0) return OBG_OK;
+  if (!frames || !cube_bits || !mask) return set_err(OBG_EINVAL, "null buffer");
+  cudaStream_t st = as_stream(stream);
+  if (mask_format == OBG_MASK_PACKED)
+    return classify_dispatch<OUT_PACKED>(frames, n_frames, height, width, levels, grid_rows, grid_cols, cube_bits,
+                                         mask, nullptr, st);
+  return classify_dispatch<OUT_U8>(frames, n_frames, height, width, levels, grid_rows, grid_cols, cube_bits, mask,
+                                   nullptr, st);
+}
+
+int obg_classify_confusion(const uint8_t* frames, int n_frames, int height, int width, int levels, int grid_rows,
+                           int grid_cols, const uint32_t* cube_bits, const uint8_t* truth, int truth_format,
+                           uint64_t* counts, void* stream) {
+  g_err[0] = 0;
+  if (int rc = classify_args(n_frames, height, width, levels, grid_rows, grid_cols, truth_format)) return rc;
+  if (n_frames == 0) return OBG_OK;
+  if (!frames || !cube_bits || !truth || !counts) return set_err(OBG_EINVAL, "null buffer");
+  cudaStream_t st = as_stream(stream);
+  uint8_t* t = const_cast<uint8_t*>(truth);                  // read only (OUT_CONF_*)
+  unsigned long long* c = reinterpret_cast<unsigned long long*>(counts);
+  if (truth_format == OBG_MASK_PACKED)
+    return classify_dispatch<OUT_CONF_PACKED>(frames, n_frames, height, width, levels, grid_rows, grid_cols,
+                                              cube_bits, t, c, st);
+  return classify_dispatch<OUT_CONF_U8>(frames, n_frames, height, width, levels, grid_rows, grid_cols, cube_bits, t,
+                                        c, st);
 }
 
 int64_t obg_serialize_workspace_bytes(int levels) {

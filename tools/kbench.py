@@ -1,6 +1,6 @@
 """Micro-benchmark of individual kernels on synthetic inputs (CUDA events).
 
-    python tools/kbench.py build|classify [--frames N] [--scene c3|const|repeat|uniform] [--levels L]
+    python tools/kbench.py build|model|classify|confusion [--frames N] [--scene c3|const|repeat|uniform] [--levels L]
 """
 import argparse
 import os
@@ -44,7 +44,7 @@ def timeit(fn, reps=20):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["build", "classify", "model"])
+    ap.add_argument("what", choices=["build", "classify", "model", "confusion"])
     ap.add_argument("--frames", type=int, default=64)
     ap.add_argument("--scene", default="c3")
     ap.add_argument("--levels", type=int, default=6)
@@ -56,12 +56,16 @@ def main():
         ms = timeit(lambda: obg.build_presence(f, a.levels))
     elif a.what == "model":
         ms = timeit(lambda: obg.build_background_model_device(f, cfg))
+    elif a.what == "confusion":      # fused classify + evaluation against a truth mask (4 B/px)
+        model = obg.build_background_model_device(f, cfg)
+        truth = (torch.rand(f.shape[:3], device="cuda") < 0.3).to(torch.uint8)
+        ms = timeit(lambda: obg.classify_confusion(model, f, truth))
     else:
         model = obg.build_background_model_device(f, cfg)
         out = torch.empty(f.shape[:3], dtype=torch.uint8, device="cuda")
         ms = timeit(lambda: obg.classify(model, f, out=out))
     print(f"{a.what} scene={a.scene} L={a.levels} frames={a.frames}: {ms * 1000:.1f} us, "
-          f"{px / ms / 1e6:.1f} Gpx/s, {px * (3 if a.what != 'classify' else 4) / ms / 1e6:.1f} GB/s")
+          f"{px / ms / 1e6:.1f} Gpx/s, {px * (4 if a.what in ('classify', 'confusion') else 3) / ms / 1e6:.1f} GB/s")
 
 
 if __name__ == "__main__":
