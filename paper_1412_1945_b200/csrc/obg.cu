@@ -327,6 +327,14 @@ __device__ __forceinline__ uint32_t rgb_word_scalar(const uint8_t* p) {
 // (and those of a second unit) issued back to back: left to itself ptxas sinks
 // them next to their first use to save registers, which starves the memory
 // pipe (ncu r2: long-scoreboard stalls dominated classify).
+__device__ __forceinline__ void load_unit_at(const uint8_t* p, uint32_t (&w)[12]) {
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "l"(p));
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4+16];"
+               : "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]) : "l"(p));
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4+32];"
+               : "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]) : "l"(p));
+}
 __device__ __forceinline__ void load_unit(const uint8_t* __restrict__ base, int64_t u, uint32_t (&w)[12]) {
   const uint8_t* p = base + 48 * u;
   asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
@@ -734,26 +742,34 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
     // while the current one is looked up (unrolled by two so the buffers
     // swap by renaming).  Trip counts are warp-uniform (lanes past the
     // segment carry valid=false) so build_unit can branch on warp votes.
+    // 32-bit trip counts and a pointer bump per iteration: the 64-bit unit
+    // indices cost ~1.2 instructions per pixel (ncu r18).
     const int lane = threadIdx.x & 31;
     const uint32_t dummy = 4u * (Smem<L>::DUMMY + uint32_t(lane));   // byte offset
-    int64_t wv = u + threadIdx.x - lane;
+    const int64_t seg_len = seg_end - u;                               // < 2^31 (host checks units_per_cta)
+    const int32_t rel0 = int32_t(threadIdx.x) - lane;                  // warp's first unit
+    const int32_t n_it = seg_len > rel0 ? int32_t((seg_len - rel0 + BUILD_BLOCK - 1) / BUILD_BLOCK) : 0;
+    const int32_t n_full = seg_len >= rel0 + 32 ? int32_t((seg_len - rel0 - 32) / BUILD_BLOCK) + 1 : 0;
+    const int32_t n_lane = seg_len > rel0 + lane ? int32_t((seg_len - rel0 - lane + BUILD_BLOCK - 1) / BUILD_BLOCK) : 0;
+    constexpr int64_t STEP = 48 * int64_t(BUILD_BLOCK);
+    const uint8_t* fp = frames + 48 * (u + rel0 + lane);
     uint32_t wa[12], wb[12];
-    if (wv + lane < seg_end) load_unit(frames, wv + lane, wa);
-    while (wv < seg_end) {
+    if (0 < n_lane) load_unit_at(fp, wa);
+    for (int32_t k = 0; k < n_it;) {
       {
-        const int64_t wn = wv + BUILD_BLOCK;
-        if (wn + lane < seg_end) load_unit(frames, wn + lane, wb);
-        if (wv + 32 <= seg_end) build_unit<L, SMEM_BITS, COUNTS, true>(wa, bits, cnt, true, dummy);
-        else build_unit<L, SMEM_BITS, COUNTS, false>(wa, bits, cnt, wv + lane < seg_end, dummy);
-        wv = wn;
+        if (k + 1 < n_lane) load_unit_at(fp + STEP, wb);
+        if (k < n_full) build_unit<L, SMEM_BITS, COUNTS, true>(wa, bits, cnt, true, dummy);
+        else build_unit<L, SMEM_BITS, COUNTS, false>(wa, bits, cnt, k < n_lane, dummy);
+        fp += STEP;
+        ++k;
       }
-      if (wv >= seg_end) break;
+      if (k >= n_it) break;
       {
-        const int64_t wn = wv + BUILD_BLOCK;
-        if (wn + lane < seg_end) load_unit(frames, wn + lane, wa);
-        if (wv + 32 <= seg_end) build_unit<L, SMEM_BITS, COUNTS, true>(wb, bits, cnt, true, dummy);
-        else build_unit<L, SMEM_BITS, COUNTS, false>(wb, bits, cnt, wv + lane < seg_end, dummy);
-        wv = wn;
+        if (k + 1 < n_lane) load_unit_at(fp + STEP, wa);
+        if (k < n_full) build_unit<L, SMEM_BITS, COUNTS, true>(wb, bits, cnt, true, dummy);
+        else build_unit<L, SMEM_BITS, COUNTS, false>(wb, bits, cnt, k < n_lane, dummy);
+        fp += STEP;
+        ++k;
       }
     }
     if constexpr (SMEM_BITS) flush_segment<L, BUILD_BLOCK>(s_bits, ws + tree * WSW, levels_out);
@@ -1865,6 +1881,8 @@ static int launch_build_flat(const uint8_t* frames, int64_t units_per_frame, int
   int64_t per_cta = (total_units + max_ctas - 1) / max_ctas;
   const int64_t min_per_cta = int64_t(BUILD_BLOCK) * 4;
   if (per_cta < min_per_cta) per_cta = min_per_cta;
+  if (per_cta >= (int64_t(1) << 31) - 2 * BUILD_BLOCK)
+    return set_err(OBG_EUNSUPPORTED, "too many pixels per launch (%lld units per CTA)", (long long)per_cta);
   const int grid = int((total_units + per_cta - 1) / per_cta);
   if (counts)
     k_build_flat<L, SMEM, true><<<grid, BUILD_BLOCK, smem, st>>>(frames, units_per_frame, total_units, group_size,
