@@ -41,6 +41,8 @@ extern "C" {
 #define OBG_EINVAL       -1   /* bad argument (maps to ValueError) */
 #define OBG_EUNSUPPORTED -2   /* valid but unsupported configuration */
 #define OBG_ECUDA        -3   /* CUDA runtime / launch failure */
+#define OBG_EFORMAT      -4   /* malformed frame / mask file (maps to FormatError, with a byte offset) */
+#define OBG_EIO          -5   /* file system error */
 
 #define OBG_WS_ZEROED   1    /* obg_build_presence flag */
 
@@ -164,6 +166,28 @@ int64_t obg_serialize_workspace_bytes(int levels);
 int obg_serialize(const uint32_t* pyramid, int levels, int has_root, uint8_t* out,
                   int64_t out_capacity, int64_t* n_out, void* workspace,
                   int64_t workspace_bytes, void* stream);
+
+/* ---- frame ingest (host only; frame_io.py) -------------------------------
+ * Binary PPM (P6, kind 6) frames / PGM (P5, kind 5) masks with the
+ * reference's header rules, messages and byte offsets (frame_io.py:22-104).
+ *
+ * Header + payload-size check of an in-memory file.  On OBG_EFORMAT,
+ * *err_offset is the reference's FormatError offset. */
+int obg_pnm_header(const uint8_t* data, int64_t size, int kind, int64_t* width,
+                   int64_t* height, int64_t* payload, int64_t* err_offset);
+
+/* Read n same-sized files (FrameSequence.load_all, frame_io.py:157-176)
+ * straight into `out` (n x height x width x (3 | 1) bytes, e.g. pinned host
+ * memory for the overlapped H2D pipeline) with n_threads host threads
+ * (<= 0: all cores).  On error *bad_index is the first failing file. */
+int obg_read_pnm_files(const char* const* paths, int n_files, int kind, int64_t width,
+                       int64_t height, uint8_t* out, int n_threads, int* bad_index,
+                       int64_t* err_offset);
+
+/* Write n masks (u8, nonzero = foreground) as P5 PGM files of 0/255
+ * (write_mask_pgm / save_mask, frame_io.py:107-125). */
+int obg_write_pgm_masks(const uint8_t* masks, int n_masks, int64_t width, int64_t height,
+                        const char* const* paths, int n_threads);
 
 #ifdef __cplusplus
 }

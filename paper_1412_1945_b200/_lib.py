@@ -20,6 +20,8 @@ OBG_OK = 0
 OBG_EINVAL = -1
 OBG_EUNSUPPORTED = -2
 OBG_ECUDA = -3
+OBG_EFORMAT = -4
+OBG_EIO = -5
 WS_ZEROED = 1
 MASK_U8 = 0
 MASK_PACKED = 1
@@ -48,6 +50,11 @@ SIGNATURES = {
     "obg_classify_confusion": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _P, _I, _P, _P]),
     "obg_serialize_workspace_bytes": (_L, [_I]),
     "obg_serialize": (_I, [_P, _I, _I, _P, _L, ctypes.POINTER(ctypes.c_int64), _P, _L, _P]),
+    "obg_pnm_header": (_I, [_P, _L, _I, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
+                            ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
+    "obg_read_pnm_files": (_I, [ctypes.POINTER(ctypes.c_char_p), _I, _I, _L, _L, _P, _I,
+                                ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int64)]),
+    "obg_write_pgm_masks": (_I, [_P, _I, _L, _L, ctypes.POINTER(ctypes.c_char_p), _I]),
 }
 ABI_VERSION = 3
 
@@ -87,13 +94,19 @@ def load() -> ctypes.CDLL:
         return lib
 
 
-def check(rc: int) -> None:
-    """Map a libobg status code to the reference's exception conventions."""
+def check(rc: int, offset: int | None = None) -> None:
+    """Map a libobg status code to the reference's exception conventions
+    (OBG_EFORMAT -> FormatError carrying the byte ``offset``)."""
     if rc == OBG_OK:
         return
     msg = load().obg_last_error().decode(errors="replace")
     if rc == OBG_EINVAL:
         raise ValueError(msg)
+    if rc == OBG_EFORMAT:
+        from .errors import FormatError
+        raise FormatError(msg, offset)
+    if rc == OBG_EIO:
+        raise OSError(msg)
     raise ObgError(f"libobg error {rc}: {msg}")
 
 

@@ -40,6 +40,15 @@ static int set_err(int code, const char* fmt, ...) {
   return code;
 }
 
+// for the host-side frame codecs (obg_io.cpp)
+extern "C" int obg_set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
 #define CUDA_TRY(expr)                                                              \
   do {                                                                              \
     cudaError_t _e = (expr);                                                        \

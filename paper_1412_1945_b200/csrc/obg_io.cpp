@@ -1,0 +1,303 @@
+// Frame ingest for the octree background model: binary PPM (P6) frames and
+// PGM (P5) masks, read straight into caller memory (e.g. pinned host buffers
+// feeding the overlapped H2D pipeline) by a pool of host threads.
+//
+// Header rules and error messages / byte offsets restate the reference's
+// codecs (frame_io.py:22-66 header tokens, 69-77 payload checks, 80-84 P6,
+// 95-104 P5): tokens separated by whitespace (space, \t, \n, \r, \v, \f),
+// '#' comments to end of line, positive decimal width / height, maxval 255,
+// exactly one whitespace byte before the payload, no trailing data.
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+#include <sys/stat.h>
+
+#include <atomic>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/obg.h"
+
+extern "C" int obg_set_error(int code, const char* fmt, ...);   // obg.cu (thread-local message)
+
+namespace {
+
+bool is_ws(uint8_t c) { return c == ' ' || c == '\t' || c == '\n' || c == '\r' || c == 0x0b || c == 0x0c; }
+
+// Python's repr() of a bytes object (the reference formats tokens with !r).
+std::string bytes_repr(const uint8_t* p, size_t n) {
+  bool has_sq = memchr(p, '\'', n) != nullptr, has_dq = memchr(p, '"', n) != nullptr;
+  const char q = (has_sq && !has_dq) ? '"' : '\'';
+  std::string s = "b";
+  s += q;
+  for (size_t i = 0; i < n; ++i) {
+    const uint8_t c = p[i];
+    if (c == uint8_t(q) || c == '\\') { s += '\\'; s += char(c); }
+    else if (c == '\t') s += "\\t";
+    else if (c == '\n') s += "\\n";
+    else if (c == '\r') s += "\\r";
+    else if (c < 0x20 || c >= 0x7f) { char b[8]; snprintf(b, sizeof b, "\\x%02x", c); s += b; }
+    else s += char(c);
+  }
+  s += q;
+  return s;
+}
+
+std::string u128_str(unsigned __int128 v) {
+  if (v == 0) return "0";
+  std::string s;
+  while (v) { s.insert(s.begin(), char('0' + int(v % 10))); v /= 10; }
+  return s;
+}
+
+struct Err {
+  int code = OBG_OK;
+  std::string msg;
+  int64_t offset = -1;
+};
+
+struct Tok {
+  size_t start, end;
+};
+
+// next header token at/after pos; false + err on failure (frame_io.py:22-41)
+bool next_token(const uint8_t* d, size_t n, size_t& pos, Tok& t, Err& e) {
+  while (pos < n) {
+    const uint8_t c = d[pos];
+    if (c == '#') {
+      const void* eol = memchr(d + pos, '\n', n - pos);
+      if (!eol) { e = {OBG_EFORMAT, "unterminated comment in header", int64_t(pos)}; return false; }
+      pos = size_t(static_cast<const uint8_t*>(eol) - d) + 1;
+    } else if (is_ws(c)) {
+      ++pos;
+    } else {
+      break;
+    }
+  }
+  if (pos >= n) { e = {OBG_EFORMAT, "unexpected end of header", int64_t(pos)}; return false; }
+  t.start = pos;
+  while (pos < n && !is_ws(d[pos]) && d[pos] != '#') ++pos;
+  t.end = pos;
+  return true;
+}
+
+bool all_digits(const uint8_t* p, size_t n) {
+  if (n == 0) return false;
+  for (size_t i = 0; i < n; ++i)
+    if (p[i] < '0' || p[i] > '9') return false;
+  return true;
+}
+
+// decimal token -> value (saturating above 2^100: such a size can never be satisfied)
+unsigned __int128 parse_dec(const uint8_t* p, size_t n, bool& huge) {
+  unsigned __int128 v = 0;
+  huge = false;
+  for (size_t i = 0; i < n; ++i) {
+    v = v * 10 + (p[i] - '0');
+    if (v >> 100) { huge = true; }
+  }
+  return v;
+}
+
+// header of a P6 (kind 6) / P5 (kind 5) image; `limit` = bytes available in d
+bool parse_header(const uint8_t* d, size_t n, int kind, int64_t& w, int64_t& h, size_t& payload, Err& e) {
+  size_t pos = 0;
+  Tok t;
+  if (!next_token(d, n, pos, t, e)) return false;
+  const char magic[3] = {'P', char('0' + kind), 0};
+  if (t.end - t.start != 2 || memcmp(d + t.start, magic, 2) != 0) {
+    e = {OBG_EFORMAT, "bad magic " + bytes_repr(d + t.start, t.end - t.start) + ", expected " +
+                          bytes_repr(reinterpret_cast<const uint8_t*>(magic), 2), int64_t(t.start)};
+    return false;
+  }
+  int64_t dims[2];
+  const char* names[2] = {"width", "height"};
+  for (int k = 0; k < 2; ++k) {
+    if (!next_token(d, n, pos, t, e)) return false;
+    if (!all_digits(d + t.start, t.end - t.start)) {
+      e = {OBG_EFORMAT, std::string("malformed ") + names[k] + " " + bytes_repr(d + t.start, t.end - t.start),
+           int64_t(t.start)};
+      return false;
+    }
+    bool huge;
+    const unsigned __int128 v = parse_dec(d + t.start, t.end - t.start, huge);
+    if (v == 0) {
+      e = {OBG_EFORMAT, std::string(names[k]) + " must be positive, got 0", int64_t(t.start)};
+      return false;
+    }
+    if (huge || v > (unsigned __int128)(int64_t(1) << 40)) {
+      e = {OBG_EUNSUPPORTED, std::string(names[k]) + " too large", int64_t(t.start)};
+      return false;
+    }
+    dims[k] = int64_t(v);
+  }
+  if (!next_token(d, n, pos, t, e)) return false;
+  if (!all_digits(d + t.start, t.end - t.start)) {
+    e = {OBG_EFORMAT, "malformed maxval " + bytes_repr(d + t.start, t.end - t.start), int64_t(t.start)};
+    return false;
+  }
+  bool huge;
+  const unsigned __int128 mv = parse_dec(d + t.start, t.end - t.start, huge);
+  if (huge || mv != 255) {
+    e = {OBG_EFORMAT, "unsupported maxval " + (huge ? std::string(reinterpret_cast<const char*>(d + t.start),
+                                                                    t.end - t.start)
+                                                      : u128_str(mv)),
+         int64_t(t.start)};
+    return false;
+  }
+  if (pos >= n || !is_ws(d[pos])) {
+    e = {OBG_EFORMAT, "missing whitespace before pixel data", int64_t(pos)};
+    return false;
+  }
+  w = dims[0];
+  h = dims[1];
+  payload = pos + 1;
+  return true;
+}
+
+// payload size checks (frame_io.py:69-77) given the total size
+bool check_payload(size_t total, size_t payload, int64_t expected, Err& e) {
+  const size_t have = total > payload ? total - payload : 0;
+  if (int64_t(have) < expected) {
+    e = {OBG_EFORMAT, "truncated pixel data: need " + std::to_string(expected) + " bytes, have " +
+                          std::to_string(have), int64_t(payload)};
+    return false;
+  }
+  if (int64_t(have) > expected) {
+    e = {OBG_EFORMAT, "trailing data after pixel payload", int64_t(payload) + expected};
+    return false;
+  }
+  return true;
+}
+
+int report(const Err& e, int64_t* err_offset) {
+  if (err_offset) *err_offset = e.offset;
+  return obg_set_error(e.code, "%s", e.msg.c_str());
+}
+
+// One file: header from its first bytes (whole file if the header is longer),
+// payload read straight into dst.  kind 6: w*h*3 bytes, kind 5: w*h bytes.
+bool read_one(const char* path, int kind, int64_t want_w, int64_t want_h, uint8_t* dst, Err& e) {
+  FILE* f = fopen(path, "rb");
+  if (!f) { e = {OBG_EIO, std::string("cannot open ") + path, -1}; return false; }
+  struct stat st;
+  if (fstat(fileno(f), &st) != 0) { fclose(f); e = {OBG_EIO, std::string("cannot stat ") + path, -1}; return false; }
+  const size_t total = size_t(st.st_size);
+  std::vector<uint8_t> head(total < 4096 ? total : 4096);
+  size_t got = fread(head.data(), 1, head.size(), f);
+  int64_t w = 0, h = 0;
+  size_t payload = 0;
+  Err he;
+  bool ok = parse_header(head.data(), got, kind, w, h, payload, he);
+  if (!ok && got < total) {
+    // the header may not fit the first block (long comments; a token cut at
+    // the block end): parse it from the whole file
+    head.resize(total);
+    got += fread(head.data() + got, 1, total - got, f);
+    ok = parse_header(head.data(), got, kind, w, h, payload, he);
+  }
+  if (!ok) { fclose(f); e = he; return false; }
+  const int64_t expected = w * h * (kind == 6 ? 3 : 1);
+  if (!check_payload(total, payload, expected, e)) { fclose(f); return false; }
+  if (w != want_w || h != want_h) {
+    fclose(f);
+    e = {OBG_EINVAL, "frame " + std::string(path) + " is " + std::to_string(w) + "x" + std::to_string(h) +
+                         ", sequence is " + std::to_string(want_w) + "x" + std::to_string(want_h), -1};
+    return false;
+  }
+  // payload bytes already in the header block, then the rest straight into dst
+  size_t have = got > payload ? got - payload : 0;
+  if (have > size_t(expected)) have = size_t(expected);
+  memcpy(dst, head.data() + payload, have);
+  if (have < size_t(expected)) {
+    if (fseek(f, long(payload + have), SEEK_SET) != 0 ||
+        fread(dst + have, 1, size_t(expected) - have, f) != size_t(expected) - have) {
+      fclose(f);
+      e = {OBG_EIO, std::string("short read from ") + path, -1};
+      return false;
+    }
+  }
+  fclose(f);
+  return true;
+}
+
+template <class F>
+void parallel_for(int n, int n_threads, F&& fn) {
+  if (n_threads <= 0) n_threads = int(std::thread::hardware_concurrency());
+  if (n_threads < 1) n_threads = 1;
+  if (n_threads > n) n_threads = n;
+  std::atomic<int> next{0};
+  auto work = [&]() {
+    for (int i = next.fetch_add(1); i < n; i = next.fetch_add(1)) fn(i);
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < n_threads; ++t) pool.emplace_back(work);
+  work();
+  for (auto& t : pool) t.join();
+}
+
+}  // namespace
+
+extern "C" {
+
+int obg_pnm_header(const uint8_t* data, int64_t size, int kind, int64_t* width, int64_t* height,
+                   int64_t* payload, int64_t* err_offset) {
+  if (kind != 5 && kind != 6) return obg_set_error(OBG_EINVAL, "kind must be 5 (PGM) or 6 (PPM)");
+  if (!data && size > 0) return obg_set_error(OBG_EINVAL, "null buffer");
+  Err e;
+  int64_t w = 0, h = 0;
+  size_t p = 0;
+  if (!parse_header(data, size_t(size), kind, w, h, p, e)) return report(e, err_offset);
+  if (!check_payload(size_t(size), p, w * h * (kind == 6 ? 3 : 1), e)) return report(e, err_offset);
+  *width = w;
+  *height = h;
+  *payload = int64_t(p);
+  return OBG_OK;
+}
+
+int obg_read_pnm_files(const char* const* paths, int n_files, int kind, int64_t width, int64_t height, uint8_t* out,
+                       int n_threads, int* bad_index, int64_t* err_offset) {
+  if (kind != 5 && kind != 6) return obg_set_error(OBG_EINVAL, "kind must be 5 (PGM) or 6 (PPM)");
+  if (n_files < 0 || width < 1 || height < 1) return obg_set_error(OBG_EINVAL, "bad sizes");
+  if (n_files == 0) return OBG_OK;
+  if (!paths || !out) return obg_set_error(OBG_EINVAL, "null buffer");
+  const int64_t frame_bytes = width * height * (kind == 6 ? 3 : 1);
+  std::vector<Err> errs(static_cast<size_t>(n_files));
+  parallel_for(n_files, n_threads, [&](int i) {
+    read_one(paths[i], kind, width, height, out + int64_t(i) * frame_bytes, errs[size_t(i)]);
+  });
+  for (int i = 0; i < n_files; ++i) {
+    if (errs[size_t(i)].code != OBG_OK) {
+      if (bad_index) *bad_index = i;
+      return report(errs[size_t(i)], err_offset);
+    }
+  }
+  return OBG_OK;
+}
+
+int obg_write_pgm_masks(const uint8_t* masks, int n_masks, int64_t width, int64_t height, const char* const* paths,
+                        int n_threads) {
+  if (n_masks < 0 || width < 1 || height < 1) return obg_set_error(OBG_EINVAL, "bad sizes");
+  if (n_masks == 0) return OBG_OK;
+  if (!masks || !paths) return obg_set_error(OBG_EINVAL, "null buffer");
+  const int64_t P = width * height;
+  std::vector<int> fail(static_cast<size_t>(n_masks), 0);
+  parallel_for(n_masks, n_threads, [&](int i) {
+    char head[64];
+    const int hn = snprintf(head, sizeof head, "P5\n%lld %lld\n255\n", (long long)width, (long long)height);
+    std::vector<uint8_t> body(static_cast<size_t>(P));
+    const uint8_t* m = masks + int64_t(i) * P;
+    for (int64_t k = 0; k < P; ++k) body[size_t(k)] = m[k] ? 255 : 0;
+    FILE* f = fopen(paths[i], "wb");
+    if (!f || fwrite(head, 1, size_t(hn), f) != size_t(hn) || fwrite(body.data(), 1, body.size(), f) != body.size())
+      fail[size_t(i)] = 1;
+    if (f && fclose(f) != 0) fail[size_t(i)] = 1;
+  });
+  for (int i = 0; i < n_masks; ++i)
+    if (fail[size_t(i)]) return obg_set_error(OBG_EIO, "cannot write %s", paths[i]);
+  return OBG_OK;
+}
+
+}  // extern "C"

@@ -69,18 +69,29 @@ def process_batches(train_host, test_host, config: ModelConfig, out_host=None, c
     """
     t = _device.torch()
     dev = t.device("cuda", t.cuda.current_device())
-    n, h, w = int(test_host.shape[0]), int(test_host.shape[1]), int(test_host.shape[2])
-    shape = (n, (h * w + 7) // 8) if packed else (n, h, w)
-    if out_host is None:
-        out_host = t.empty(shape, dtype=t.uint8, pin_memory=True)
     main = t.cuda.current_stream()
-    up, down = t.cuda.Stream(), t.cuda.Stream()
-    # training frames + model
+    up = t.cuda.Stream()
     with t.cuda.stream(up):
         train = train_host.to(dev, non_blocking=True)
     main.wait_stream(up)
     train.record_stream(main)
     model = build_background_model_device(train, config)
+    return model, classify_host(model, test_host, out_host=out_host, chunk=chunk, packed=packed, up=up)
+
+
+def classify_host(model: BackgroundModel, test_host, out_host=None, chunk: int = 32, packed: bool = False, up=None):
+    """Masks of host frames with H2D / classify / D2H overlapped chunk by chunk
+    (see ``process_batches``).  Returns ``out_host`` (pinned if allocated here);
+    the copies are complete when the current stream is."""
+    t = _device.torch()
+    dev = t.device("cuda", t.cuda.current_device())
+    n, h, w = int(test_host.shape[0]), int(test_host.shape[1]), int(test_host.shape[2])
+    shape = (n, (h * w + 7) // 8) if packed else (n, h, w)
+    if out_host is None:
+        out_host = t.empty(shape, dtype=t.uint8, pin_memory=True)
+    main = t.cuda.current_stream()
+    up = up if up is not None else t.cuda.Stream()
+    down = t.cuda.Stream()
     # test chunks: double-buffered device frames / masks
     chunk = max(1, min(chunk, n))
     frames = [t.empty((chunk, h, w, 3), dtype=t.uint8, device=dev) for _ in range(2)]
@@ -109,4 +120,55 @@ def process_batches(train_host, test_host, config: ModelConfig, out_host=None, c
             drained[b].record(down)
     main.wait_stream(down)
     main.wait_stream(up)
-    return model, out_host
+    return out_host
+
+
+def detect_sequence(sequence, config: ModelConfig, out_dir=None, batch: int = 64, chunk: int = 16,
+                    threads: int = 0):
+    """Directory of PPM frames -> background model + foreground masks (SURVEY.md
+    §8(f) row 2: the ingest pipeline around the hot path).
+
+    The first ``config.training_frames`` frames (whole groups) build the model;
+    then every frame is classified.  Frames are read by host threads straight
+    into pinned buffers (``FrameSequence.load_batch``), batch ``i + 1`` is read
+    while batch ``i`` goes through the overlapped H2D / classify / D2H chunks,
+    and with ``out_dir`` the masks of batch ``i`` are written as 0/255 PGM
+    files (``<frame name>.pgm``) by host threads, also in the background.
+    Returns (model, masks) -- masks a (n, h, w) uint8 0/1 host tensor -- or
+    (model, None) when writing to ``out_dir``.
+    """
+    from concurrent.futures import ThreadPoolExecutor
+    from pathlib import Path
+    from .frame_io import FrameSequence, save_masks
+    t = _device.torch()
+    seq = sequence if isinstance(sequence, FrameSequence) else FrameSequence.scan(sequence)
+    n = len(seq)
+    n_train = (min(n, config.training_frames) // config.group_size) * config.group_size
+    if n_train == 0:
+        raise ValueError(f"need at least {config.group_size} frames for one group, got {n}")
+    dev = t.device("cuda", t.cuda.current_device())
+    train = seq.load_batch(range(n_train), threads=threads).to(dev, non_blocking=True)
+    model = build_background_model_device(train, config)
+    out = None if out_dir is not None else t.empty((n, seq.height, seq.width), dtype=t.uint8, pin_memory=True)
+    if out_dir is not None:
+        Path(out_dir).mkdir(parents=True, exist_ok=True)
+    starts = list(range(0, n, batch))
+    with ThreadPoolExecutor(max_workers=2) as pool:
+        nxt = pool.submit(seq.load_batch, range(starts[0], min(n, starts[0] + batch)), None, True, threads)
+        writing = None
+        for i, s0 in enumerate(starts):
+            frames = nxt.result()
+            if i + 1 < len(starts):
+                s1 = starts[i + 1]
+                nxt = pool.submit(seq.load_batch, range(s1, min(n, s1 + batch)), None, True, threads)
+            dst = out[s0:s0 + len(frames)] if out is not None else None
+            masks = classify_host(model, frames, out_host=dst, chunk=chunk)
+            t.cuda.current_stream().synchronize()
+            if out_dir is not None:
+                if writing is not None:
+                    writing.result()
+                paths = [Path(out_dir) / (Path(seq.names[s0 + j]).stem + ".pgm") for j in range(len(frames))]
+                writing = pool.submit(save_masks, masks, paths, threads)
+        if writing is not None:
+            writing.result()
+    return model, out
