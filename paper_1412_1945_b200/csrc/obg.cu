@@ -1270,7 +1270,7 @@ k_levels_cube(uint32_t* __restrict__ ws, int L) {
 // word comes from the workspace (leaf cube, then upper levels) and is zeroed
 // after reading.  Merged leaf words go to the classify operand, merged upper
 // words to `pyr` (region r at r * PW, level_offset layout) for K4.
-constexpr int MERGE_GROUPS_C = 16;
+constexpr int MERGE_GROUPS_C = 8;      // 8 trees per thread at C3 (16 groups: +0.4 us, 32: +5 us; r20)
 __global__ void __launch_bounds__(32 * MERGE_GROUPS_C)
 k_merge_cube(uint32_t* __restrict__ pyr, uint32_t* __restrict__ ws, int n_groups, int n_regions, int L,
              int64_t k_min, uint32_t* __restrict__ cube) {
@@ -1365,20 +1365,39 @@ k_merge_cube(uint32_t* __restrict__ pyr, uint32_t* __restrict__ ws, int n_groups
 }
 
 // K4: merged path-order pyramid words from the merged cube-order levels
-// (levels < L in group 0's scratch slot, level L in the operand).
+// (levels < L in `pyr`, level L in the operand).  Eight threads per word,
+// one nibble gather each, OR-combined by shuffles: 8x the threads of a
+// word-per-thread kernel for this latency-bound pass.  Grid (word blocks,
+// regions).
 __global__ void __launch_bounds__(256)
 k_morton_merged(const uint32_t* __restrict__ pyr, const uint32_t* __restrict__ cube, int n_regions, int L,
                 uint32_t* __restrict__ out) {
   const int64_t PW = pyr_words(L), OW = operand_words(L);
-  const int64_t total = PW * n_regions;
-  for (int64_t wi = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; wi < total;
-       wi += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t r = wi / PW, w = wi - r * PW;
+  const int64_t r = blockIdx.y;
+  const int64_t g = int64_t(blockIdx.x) * 256 + threadIdx.x;
+  const int64_t w = g >> 3;
+  const uint32_t c = uint32_t(g & 7);
+  uint32_t part = 0;
+  if (w < PW) {
     int l = 1;
-    while (l < L && w >= level_offset(l + 1)) ++l;
-    const uint32_t* src = (l == L) ? cube + r * OW : pyr + r * PW + level_offset(l);
-    out[wi] = morton_word_from_cube(src, uint32_t(w - level_offset(l)), l);
+    int64_t off = 0, next = level_words(1);
+    while (l < L && w >= next) { off = next; ++l; next += level_words(l); }
+    const uint32_t* src = (l == L) ? cube + r * OW : pyr + r * PW + off;
+    const uint32_t m = uint32_t(w - off);
+    if (l == 1) {
+      part = c == 0 ? (src[0] & 0xFFu) : 0u;         // cube index == path code at level 1
+    } else {
+      const uint32_t base = code_to_cube(m << 5, l);
+      const uint32_t g0 = c & 1, r0 = (c >> 1) & 1, g1 = (c >> 2) & 1;
+      const uint32_t idx = base + ((g0 | (g1 << 1)) << l) + (r0 << (2 * l));
+      const uint32_t nib = (src[idx >> 5] >> (idx & 31u)) & 0xFu;
+      part = ((nib & 3u) | ((nib & 12u) << 6)) << (g0 * 2 + r0 * 4 + g1 * 16);
+    }
   }
+  part |= __shfl_xor_sync(0xFFFFFFFFu, part, 1);
+  part |= __shfl_xor_sync(0xFFFFFFFFu, part, 2);
+  part |= __shfl_xor_sync(0xFFFFFFFFu, part, 4);
+  if (c == 0 && w < PW) out[r * PW + w] = part;
 }
 
 __global__ void __launch_bounds__(256)
@@ -2045,8 +2064,8 @@ int obg_build_model(const uint8_t* frames, int n_frames, int height, int width, 
   k_merge_cube<<<dim3(unsigned((pyr_words(levels) + 31) / 32), unsigned(n_regions)), dim3(32, MERGE_GROUPS_C), 0, st>>>(
       tree_pyramids, static_cast<uint32_t*>(workspace), n_groups, int(n_regions), levels, k_min, out_cube);
   LAUNCH_CHECK("k_merge_cube");
-  k_morton_merged<<<grid_for(words, 256, sm_count() * 8), 256, 0, st>>>(tree_pyramids, out_cube, int(n_regions),
-                                                                         levels, out_merged);
+  k_morton_merged<<<dim3(unsigned((pyr_words(levels) * 8 + 255) / 256), unsigned(n_regions)), 256, 0, st>>>(
+      tree_pyramids, out_cube, int(n_regions), levels, out_merged);
   LAUNCH_CHECK("k_morton_merged");
   return finish_operand(out_cube, n_regions, levels, st);
 }

@@ -414,3 +414,18 @@ def test_build_model_groups_and_repeat(cuda):
         for _ in range(3):
             model = obg.build_background_model_device(dev, cfg)
             assert model.trees[0][0].to_bytes() == orc.to_bytes(want[(0, 0)])
+
+
+@pytest.mark.gpu
+def test_build_model_many_trees(cuda):
+    """> 8 x 252 trees per merge: the byte counters of k_merge_cube spill into
+    the 32-bit shared counters (the `wide` path)."""
+    rng = np.random.default_rng(8)
+    n = 2100
+    base = rng.integers(0, 256, size=(1, 1, 1, 3))
+    frames = np.clip(base + rng.integers(-40, 41, size=(n, 8, 16, 3)), 0, 255).astype(np.uint8)
+    for levels, thr in [(4, 0.5), (5, 0.05), (3, 0.99)]:
+        cfg = ModelConfig(levels=levels, threshold=thr, training_frames=n)
+        model = obg.build_background_model_device(cuda.from_numpy(frames).cuda(), cfg)
+        want = orc.build_background_model(list(frames), levels, thr)
+        assert model.trees[0][0].to_bytes() == orc.to_bytes(want[(0, 0)])
