@@ -222,6 +222,13 @@ struct SmemT {
   __host__ __device__ static constexpr uint32_t compact_word(uint32_t i) {
     return split && i >= ROWS ? i - ROWS + HALF : i;
   }
+  // the data words only (no pads): index i -> shared word
+  static constexpr uint32_t data_words = skew ? (split ? 2u : 1u) * (1u << L) * (GW << L) : uint32_t(words);
+  __host__ __device__ static constexpr uint32_t data_word(uint32_t i) {
+    if constexpr (!skew) return i;
+    else if constexpr (split) return (i >> 12) * HALF + ((i >> 6) & 63u) * ROWW + (i & 63u);
+    else return (i / (GW << L)) * ROWW + (i % (GW << L));
+  }
   // shared word p -> (half, R', column); column >= GW * 2^L is a pad word
   __device__ static void locate(uint32_t p, uint32_t& h, uint32_t& r, uint32_t& c) {
     h = split && p >= HALF ? 1u : 0u;
@@ -675,17 +682,14 @@ __device__ __forceinline__ void build_unit(const uint32_t (&w)[12], uint32_t* bi
 // path-order ones here cost 5.5x K1's flush (ncu r8), which is why those
 // are made once, for the merged model.  Leaves the bitset zeroed.
 template <int L, int NT>
-__device__ __forceinline__ void flush_segment(uint32_t* s_bits, uint32_t* dst, int levels_out) {
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < Smem<L>::compact; i += NT) {
-    const uint32_t p = Smem<L>::compact_word(i);
-    const uint32_t x = s_bits[p];
-    if (x) flush_smem_word<L>(dst, p, x);
-  }
+__device__ __forceinline__ void flush_segment(uint32_t* s_bits, uint32_t* dst, int levels_out, bool last) {
+  __syncthreads();                                   // the segment's bitset is complete
+  uint32_t* up = dst + cube_words(L);
+  uint32_t* sc = s_bits + Smem<L>::SCRATCH;
+  const bool levels = L >= 2 && levels_out;
+  // phase A: level L-1 from the bitset (read only)
   if constexpr (L >= 2) {
-    if (levels_out) {
-      uint32_t* up = dst + cube_words(L);
-      uint32_t* sc = s_bits + Smem<L>::SCRATCH;
+    if (levels) {
       constexpr uint32_t NW = uint32_t(level_words(L - 1));
       constexpr uint32_t OFF = uint32_t(level_offset(L - 1));
       for (uint32_t pw = threadIdx.x; pw < NW; pw += NT) {
@@ -694,6 +698,20 @@ __device__ __forceinline__ void flush_segment(uint32_t* s_bits, uint32_t* dst, i
         if (v) atomicOr(up + OFF + pw, v);
       }
       __syncthreads();
+    }
+  }
+  // phase B: OR the non-zero leaf words into the tree's cube and clear them
+  // (data words only; the pads stay 0), with level L-2 from the scratch
+  for (uint32_t i = threadIdx.x; i < Smem<L>::data_words; i += NT) {
+    const uint32_t p = Smem<L>::data_word(i);
+    const uint32_t x = s_bits[p];
+    if (x) {
+      flush_smem_word<L>(dst, p, x);
+      if (!last) s_bits[p] = 0u;
+    }
+  }
+  if constexpr (L >= 3) {
+    if (levels) {
       for (int l = L - 2; l >= 1; --l) {
         const uint32_t nw = uint32_t(level_words(l)), off = uint32_t(level_offset(l));
         const uint32_t* child = sc + level_offset(l + 1);
@@ -704,14 +722,10 @@ __device__ __forceinline__ void flush_segment(uint32_t* s_bits, uint32_t* dst, i
         }
         __syncthreads();
       }
-    } else {
-      __syncthreads();
+      return;
     }
-  } else {
-    __syncthreads();
   }
-  for (uint32_t i = threadIdx.x; i < Smem<L>::compact; i += NT) s_bits[Smem<L>::compact_word(i)] = 0u;
-  __syncthreads();
+  __syncthreads();                                   // bitset clear before the next segment
 }
 
 template <int L, bool SMEM_BITS, bool COUNTS>
@@ -781,7 +795,7 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
         ++k;
       }
     }
-    if constexpr (SMEM_BITS) flush_segment<L, BUILD_BLOCK>(s_bits, ws + tree * WSW, levels_out);
+    if constexpr (SMEM_BITS) flush_segment<L, BUILD_BLOCK>(s_bits, ws + tree * WSW, levels_out, seg_end >= u_end);
     u = seg_end;
   }
 }
