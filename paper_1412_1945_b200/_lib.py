@@ -14,7 +14,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_build", "libobg.so")
+# OBG_LIB_PATH: an alternative build of the same library (A/B kernel experiments, tools/ab.py)
+LIB_PATH = os.environ.get("OBG_LIB_PATH") or os.path.join(_HERE, "_build", "libobg.so")
 
 OBG_OK = 0
 OBG_EINVAL = -1

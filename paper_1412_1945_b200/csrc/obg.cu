@@ -343,12 +343,15 @@ __device__ __forceinline__ uint32_t rgb_word_scalar(const uint8_t* p) {
 // (and those of a second unit) issued back to back: left to itself ptxas sinks
 // them next to their first use to save registers, which starves the memory
 // pipe (ncu r2: long-scoreboard stalls dominated classify).
+#ifndef OBG_LD_HINT
+#define OBG_LD_HINT ""
+#endif
 __device__ __forceinline__ void load_unit_at(const uint8_t* p, uint32_t (&w)[12]) {
-  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+  asm volatile("ld.global.nc" OBG_LD_HINT ".v4.u32 {%0, %1, %2, %3}, [%4];"
                : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "l"(p));
-  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4+16];"
+  asm volatile("ld.global.nc" OBG_LD_HINT ".v4.u32 {%0, %1, %2, %3}, [%4+16];"
                : "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]) : "l"(p));
-  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4+32];"
+  asm volatile("ld.global.nc" OBG_LD_HINT ".v4.u32 {%0, %1, %2, %3}, [%4+32];"
                : "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]) : "l"(p));
 }
 __device__ __forceinline__ void load_unit(const uint8_t* __restrict__ base, int64_t u, uint32_t (&w)[12]) {
@@ -393,7 +396,13 @@ static int occupancy(K kernel, int block, size_t smem) {
 // cube bitset (check-before-set: an ATOMS only when the bit is new to this
 // CTA), and ORs the non-zero words into the tree's workspace bitset whenever
 // its range crosses a tree (group) boundary.
-constexpr int BUILD_BLOCK = 512;
+#ifndef OBG_BUILD_BLOCK
+#define OBG_BUILD_BLOCK 1024
+#endif
+#ifndef OBG_BUILD_MINB
+#define OBG_BUILD_MINB (1024 / OBG_BUILD_BLOCK)
+#endif
+constexpr int BUILD_BLOCK = OBG_BUILD_BLOCK;
 
 template <int L, bool SMEM_BITS>
 __device__ __forceinline__ void set_bit(uint32_t* bits, uint32_t idx) {
@@ -463,7 +472,14 @@ __device__ __forceinline__ void pair_positions(const uint32_t (&w)[12], uint32_t
   constexpr uint32_t selG = uint32_t(b + 1) | (uint32_t(b + 2) << 4) | (uint32_t(b + 4) << 8) | (uint32_t(b + 5) << 12);
   const uint32_t yR = __byte_perm(w[a], w[a + 1], selR);
   const uint32_t yG = __byte_perm(w[a], w[a + 1], selG);
-  const uint32_t P = __umulhi(yR, 1u << (32 - s)) & (M | (M << 16));           // R'_A | R'_B << 16
+  // R' x row stride: when the stride is a multiple of 2^s the truncation
+  // shift folds into the multiplier, (R & ~(2^s-1)) x stride / 2^s -- one
+  // mask instead of a multiply-high and a mask
+  constexpr bool fold = ((LY::ROWW * 4u) % (1u << s)) == 0;
+  constexpr uint32_t RMUL = fold ? (LY::ROWW * 4u) >> s : LY::ROWW * 4u;
+  uint32_t P;
+  if constexpr (fold) P = yR & ((M << s) | (M << (s + 16)));                     // R_A & ~3 | R_B & ~3 << 16
+  else P = __umulhi(yR, 1u << (32 - s)) & (M | (M << 16));                       // R'_A | R'_B << 16
   uint32_t q;
   if constexpr (LY::split) {
     q = (yG & 0x80FC80FCu) | obase2;                                             // G & 0xFC | (B & 0x80) << 8
@@ -476,7 +492,7 @@ __device__ __forceinline__ void pair_positions(const uint32_t (&w)[12], uint32_t
     if constexpr (L == 6) t |= __umulhi(yG, 1u << 19) & 0x00040004u;           // B'5 (bits 15, 31) -> 2, 18
     q = (g & ((M << gpos) | (M << (gpos + 16)))) | t;
   }
-  const uint32_t pair = P * (LY::ROWW * 4u) + q;
+  const uint32_t pair = P * RMUL + q;
   addr_b = __umulhi(pair, 1u << 16);
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(addr_a) : "r"(addr_b), "r"(0xFFFF0000u), "r"(pair));   // pair & 0xFFFF
   bsel_a = __umulhi(yG, 1u << (24 - s));                                         // B_A' in the low bits
@@ -601,6 +617,20 @@ __device__ __forceinline__ uint32_t lds_at(uint32_t off) {
 __device__ __forceinline__ void reds_or_at(uint32_t off, uint32_t v) {
   asm volatile("red.shared.or.b32 [%0+1024], %1;" :: "r"(off), "r"(v) : "memory");
 }
+// red.shared.or at [off] only in the lanes where `hit` is 0 (a predicated ATOMS)
+__device__ __forceinline__ void reds_or_if(uint32_t off, uint32_t v, uint32_t hit) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %2, 0;\n\t@p red.shared.or.b32 [%0+1024], %1;\n\t}"
+               :: "r"(off), "r"(v), "r"(hit) : "memory");
+}
+
+// bit 0 of v0 & v1 & v2 & v3 in two LOP3s (plain C++ lets ptxas share the
+// v & 1 terms with the rare path and spend a third)
+__device__ __forceinline__ bool all_hit4(const uint32_t (&v)[4]) {
+  uint32_t t, u;
+  asm("lop3.b32 %0, %1, %2, %3, 0x80;" : "=r"(t) : "r"(v[0]), "r"(v[1]), "r"(v[2]));
+  asm("lop3.b32 %0, %1, %2, 1, 0x80;" : "=r"(u) : "r"(t), "r"(v[3]));
+  return u != 0u;
+}
 
 // One 16-pixel unit, called by all 32 lanes of a warp (`valid` false for
 // lanes past the segment).  Lookups go in groups of four; a group takes the
@@ -637,25 +667,16 @@ __device__ __forceinline__ void build_unit(const uint32_t (&w)[12], uint32_t* bi
       v[j] = __funnelshift_r(wd, wd, bsel[j]);
     }
     if constexpr (SMEM_BITS) {
-      // warp-uniform skip; otherwise every lane issues four atomics, those
-      // of pixels that did not miss aimed at the lane's private dummy word:
-      // no per-lane branches or convergence barriers around the rare path
-      // Which of the four lookups missed in some lane (one REDUX): only
-      // those issue atomics -- a slow group usually has one miss among 128
-      // pixels, and shared atomics are the costliest MIO traffic (ncu r16:
-      // the MIO queue, not memory latency, throttles this kernel).
-      const bool miss = valid && !(v[0] & v[1] & v[2] & v[3] & 1u);
+      // Warp-uniform skip of the common all-hit group.  A slow group (about
+      // a third of them at C3: first sightings of a leaf within the CTA's
+      // segment are ~0.46 % of pixels, tools/sim_misses.py) issues four
+      // predicated atomics, each landing only in the lanes that missed that
+      // pixel: three instructions per pixel, no vote-reduce, no branches
+      // per pixel (the REDUX + select version cost ~26 per slow group).
+      const bool miss = valid && !all_hit4(v);
       if (__any_sync(0xFFFFFFFFu, miss)) {
-        const uint32_t mm = valid ? ((~v[0] & 1u) | ((~v[1] & 1u) << 1) | ((~v[2] & 1u) << 2) | ((~v[3] & 1u) << 3))
-                                  : 0u;
-        const uint32_t rm = __reduce_or_sync(0xFFFFFFFFu, mm);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (rm & (1u << j)) {
-            const uint32_t o = (mm & (1u << j)) ? addr[j] : dummy;
-            reds_or_at(o, Smem<L>::set_mask(bsel[j]));
-          }
-        }
+        for (int j = 0; j < 4; ++j) reds_or_if(addr[j], Smem<L>::set_mask(bsel[j]), valid ? (v[j] & 1u) : 1u);
       }
     } else {
       const bool miss = valid && !(v[0] & v[1] & v[2] & v[3] & 1u);
@@ -729,7 +750,7 @@ __device__ __forceinline__ void flush_segment(uint32_t* s_bits, uint32_t* dst, i
 }
 
 template <int L, bool SMEM_BITS, bool COUNTS>
-__global__ void __launch_bounds__(BUILD_BLOCK, 2)
+__global__ void __launch_bounds__(BUILD_BLOCK, OBG_BUILD_MINB)
 k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t total_units,
              int group_size, int64_t units_per_cta, uint32_t* __restrict__ ws,
              uint32_t* __restrict__ out_pyr, int64_t n_trees, uint32_t* __restrict__ zero_cube,
@@ -776,25 +797,23 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
     const int32_t n_lane = seg_len > rel0 + lane ? int32_t((seg_len - rel0 - lane + BUILD_BLOCK - 1) / BUILD_BLOCK) : 0;
     constexpr int64_t STEP = 48 * int64_t(BUILD_BLOCK);
     const uint8_t* fp = frames + 48 * (u + rel0 + lane);
+#define OBG_BUILD_STEP(CUR, NXT)                                                              \
+    {                                                                                          \
+      if (k + STAGES - 1 < n_lane) load_unit_at(fp + (STAGES - 1) * STEP, NXT);                \
+      if (k < n_full) build_unit<L, SMEM_BITS, COUNTS, true>(CUR, bits, cnt, true, dummy);     \
+      else build_unit<L, SMEM_BITS, COUNTS, false>(CUR, bits, cnt, k < n_lane, dummy);         \
+      fp += STEP;                                                                              \
+      ++k;                                                                                     \
+    }
+    constexpr int STAGES = 2;
     uint32_t wa[12], wb[12];
     if (0 < n_lane) load_unit_at(fp, wa);
     for (int32_t k = 0; k < n_it;) {
-      {
-        if (k + 1 < n_lane) load_unit_at(fp + STEP, wb);
-        if (k < n_full) build_unit<L, SMEM_BITS, COUNTS, true>(wa, bits, cnt, true, dummy);
-        else build_unit<L, SMEM_BITS, COUNTS, false>(wa, bits, cnt, k < n_lane, dummy);
-        fp += STEP;
-        ++k;
-      }
+      OBG_BUILD_STEP(wa, wb)
       if (k >= n_it) break;
-      {
-        if (k + 1 < n_lane) load_unit_at(fp + STEP, wa);
-        if (k < n_full) build_unit<L, SMEM_BITS, COUNTS, true>(wb, bits, cnt, true, dummy);
-        else build_unit<L, SMEM_BITS, COUNTS, false>(wb, bits, cnt, k < n_lane, dummy);
-        fp += STEP;
-        ++k;
-      }
+      OBG_BUILD_STEP(wb, wa)
     }
+#undef OBG_BUILD_STEP
     if constexpr (SMEM_BITS) flush_segment<L, BUILD_BLOCK>(s_bits, ws + tree * WSW, levels_out, seg_end >= u_end);
     u = seg_end;
   }
@@ -840,16 +859,8 @@ __device__ __forceinline__ void build_unit_l7h(const uint32_t (&w)[12], uint32_t
     }
     const bool miss = valid && !(v[0] & v[1] & v[2] & v[3] & 1u);
     if (__any_sync(0xFFFFFFFFu, miss)) {
-      const uint32_t mm = valid ? ((~v[0] & 1u) | ((~v[1] & 1u) << 1) | ((~v[2] & 1u) << 2) | ((~v[3] & 1u) << 3))
-                                : 0u;
-      const uint32_t rm = __reduce_or_sync(0xFFFFFFFFu, mm);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (rm & (1u << j)) {
-          const uint32_t o = (mm & (1u << j)) ? addr[j] : dummy;
-          reds_or_at(o, 1u << (bsel[j] & 31u));
-        }
-      }
+      for (int j = 0; j < 4; ++j) reds_or_if(addr[j], 1u << (bsel[j] & 31u), valid ? (v[j] & 1u) : 1u);
     }
   }
 }

@@ -15,6 +15,18 @@ from paper_1412_1945_b200 import scenes  # noqa: E402
 
 
 def frames_for(kind, n, levels):
+    cache = f"/tmp/kbench_{kind}_{n}.npy"      # A/B runs (tools/ab.py) reuse the frames
+    if os.path.exists(cache):
+        return np.load(cache)
+    f = _frames_for(kind, n, levels)
+    try:
+        np.save(cache, f)
+    except OSError:
+        pass
+    return f
+
+
+def _frames_for(kind, n, levels):
     if kind == "c3":
         return scenes.generate(3, n_train=n, n_test=0).train
     if kind == "const":
@@ -52,10 +64,16 @@ def main():
     f = torch.from_numpy(frames_for(a.scene, a.frames, a.levels)).cuda()
     px = f.shape[0] * f.shape[1] * f.shape[2]
     cfg = obg.ModelConfig(levels=a.levels, threshold=0.5, training_frames=a.frames)
+    digest = ""
     if a.what == "build":
         ms = timeit(lambda: obg.build_presence(f, a.levels))
     elif a.what == "model":
         ms = timeit(lambda: obg.build_background_model_device(f, cfg))
+        m = obg.build_background_model_device(f, cfg)
+        import hashlib
+        h = hashlib.sha1(m._dev_pyr.cpu().numpy().tobytes())
+        h.update(m._dev_cube.cpu().numpy().tobytes())
+        digest = " model=" + h.hexdigest()[:12]
     elif a.what == "confusion":      # fused classify + evaluation against a truth mask (4 B/px)
         model = obg.build_background_model_device(f, cfg)
         truth = (torch.rand(f.shape[:3], device="cuda") < 0.3).to(torch.uint8)
@@ -65,7 +83,7 @@ def main():
         out = torch.empty(f.shape[:3], dtype=torch.uint8, device="cuda")
         ms = timeit(lambda: obg.classify(model, f, out=out))
     print(f"{a.what} scene={a.scene} L={a.levels} frames={a.frames}: {ms * 1000:.1f} us, "
-          f"{px / ms / 1e6:.1f} Gpx/s, {px * (4 if a.what in ('classify', 'confusion') else 3) / ms / 1e6:.1f} GB/s")
+          f"{px / ms / 1e6:.1f} Gpx/s, {px * (4 if a.what in ('classify', 'confusion') else 3) / ms / 1e6:.1f} GB/s{digest}")
 
 
 if __name__ == "__main__":
