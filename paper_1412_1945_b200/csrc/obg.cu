@@ -1234,12 +1234,12 @@ k_merge(const uint32_t* __restrict__ pyr, int n_trees, int n_regions, int L, int
 // a path-order word (k_pyramid: 12.9 us at C3, ncu r9).  Only the merged
 // model (one tree per region) is converted to path order, and its leaf level
 // is already the classify operand.
-//   K2c k_levels_cube  per tree: levels L-1..1 (cube order) into the scratch
-//                      tree pyramids, from the workspace cube
-//   K3c k_merge_cube   per node word: count over trees, threshold; merged
-//                      leaf level -> the classify operand, merged upper levels
-//                      -> the scratch slot of group 0; workspace zeroed
-//   K4  k_morton_merged merged levels -> path-order pyramid (out_merged)
+//   K1  k_build_flat   per tree: leaf cube + cube-order levels L-1..1 into
+//                      the workspace (its flush; k_levels_cube when K1 has no
+//                      shared bitset: L >= 7, generic grids)
+//   K3f k_merge_fused  per node word: count over trees, threshold; merged
+//                      leaf level -> the classify operand, every merged level
+//                      -> the path-order pyramid (out_merged); workspace zeroed
 // ---------------------------------------------------------------------------
 
 // Levels L-1 .. 1 of tree t (cube order) into the workspace after its leaf
@@ -1290,139 +1290,218 @@ k_levels_cube(uint32_t* __restrict__ ws, int L) {
   }
 }
 
-// K3c.  Block = 32 node words (threadIdx.x) x MERGE_GROUPS_C tree groups, SWAR
-// byte counters as in k_merge; grid = (word blocks, regions).  Every tree
-// word comes from the workspace (leaf cube, then upper levels) and is zeroed
-// after reading.  Merged leaf words go to the classify operand, merged upper
-// words to `pyr` (region r at r * PW, level_offset layout) for K4.
-constexpr int MERGE_GROUPS_C = 8;      // 8 trees per thread at C3 (16 groups: +0.4 us, 32: +5 us; r20)
-__global__ void __launch_bounds__(32 * MERGE_GROUPS_C)
-k_merge_cube(uint32_t* __restrict__ pyr, uint32_t* __restrict__ ws, int n_groups, int n_regions, int L,
-             int64_t k_min, uint32_t* __restrict__ cube) {
-  const int64_t r = blockIdx.y;
-  __shared__ uint32_t s_acc[MERGE_GROUPS_C][8][32];
-  __shared__ uint32_t s_wide[32][33];
-  __shared__ uint32_t s_bits[MERGE_GROUPS_C][32];
+// K3f block = 32 node words (threadIdx.x) x MERGE_GROUPS_C tree groups.
+#ifndef OBG_MERGE_GROUPS
+#define OBG_MERGE_GROUPS 16      // 4 trees per thread at C3: one round of loads (8 groups: +2-3 us)
+#endif
+constexpr int MERGE_GROUPS_C = OBG_MERGE_GROUPS;
+
+// K3f: merge and path-order conversion in ONE launch (it replaced a merge
+// kernel and a separate cube -> path-order kernel: two latency-bound launches
+// of ~5 and ~4 us at C3).  Levels l >= 3 are cut into tiles of 2 R' x 4 G'
+// rows (all B'): the 32 codes of a path-order word differ only in r0, g0, g1,
+// b0, b1, so every path-order word lies inside one tile, and a CTA that
+// merged a tile's cube words (tile-major, in shared memory) writes that
+// tile's path-order words itself.  Levels 1..2 (3 words) are merged and
+// converted by block 0 of each region.  Counting: 8 tree groups x 32 words,
+// SWAR byte counters (bit q + 8j of a word in byte j of acc[q]), folded into
+// 32-bit shared counters every 252 trees; the workspace is handed back zeroed.
+// Count word `off` (relative to tree 0 of the region; off < 0: no word) over
+// the trees of this thread's group and return the merged bits of the CTA's
+// 32-word slot x (valid in thread y == 0).  Zeroes what it reads.
+__device__ __forceinline__ uint32_t merge_slot(uint32_t* __restrict__ ws, int64_t off, int64_t stride, int n_groups,
+                                               int64_t k_min, uint32_t (&s_acc)[MERGE_GROUPS_C][8][32],
+                                               uint32_t (&s_wide)[32][33], uint32_t (&s_bits)[8][32], bool wide) {
   const int x = threadIdx.x, y = threadIdx.y;
-  const int64_t PW = pyr_words(L), CW = cube_words(L), OW = operand_words(L), WSW = ws_words(L);
-  const int64_t leaf_off = level_offset(L);
-  const bool wide = (n_groups + MERGE_GROUPS_C - 1) / MERGE_GROUPS_C >= 252;   // a thread may flush
-  for (int64_t base = int64_t(blockIdx.x) * 32; base < PW; base += int64_t(gridDim.x) * 32) {
-    const int64_t w = base + x;
-    const bool valid = w < PW;
-    const bool leafw = w >= leaf_off;
-    if (wide) {
-      for (int i = y * 32 + x; i < 32 * 33; i += 32 * MERGE_GROUPS_C) (&s_wide[0][0])[i] = 0;
-      __syncthreads();
-    }
-    uint32_t acc[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = 0;
-    int since = 0;
-    if (valid) {
-      uint32_t* p = ws + r * WSW + (leafw ? w - leaf_off : CW + w);
-      const int64_t stride = WSW * n_regions;
-      int t = y;
-      for (; t + 3 * MERGE_GROUPS_C < n_groups; t += 4 * MERGE_GROUPS_C) {
-        uint32_t* pa = p + int64_t(t) * stride;
-        const int64_t st = int64_t(MERGE_GROUPS_C) * stride;
-        const uint32_t a = __ldcg(pa), b = __ldcg(pa + st), d = __ldcg(pa + 2 * st), e = __ldcg(pa + 3 * st);
-        // hand the workspace back zeroed
-        if (a) pa[0] = 0u;
-        if (b) pa[st] = 0u;
-        if (d) pa[2 * st] = 0u;
-        if (e) pa[3 * st] = 0u;
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          acc[q] += ((a >> q) & 0x01010101u) + ((b >> q) & 0x01010101u) + ((d >> q) & 0x01010101u) +
-                    ((e >> q) & 0x01010101u);
-        since += 4;
-        if (since > 251) {   // keep byte counters below 256
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) atomicAdd(&s_wide[x][q + 8 * j], (acc[q] >> (8 * j)) & 0xFFu);
-            acc[q] = 0;
-          }
-          since = 0;
-        }
-      }
-      for (; t < n_groups; t += MERGE_GROUPS_C) {
-        uint32_t* pa = p + int64_t(t) * stride;
-        const uint32_t a = __ldcg(pa);
-        if (a) *pa = 0u;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) acc[q] += (a >> q) & 0x01010101u;
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 8; ++q) s_acc[y][q][x] = acc[q];
-    __syncthreads();
-    // threads y < 8: bits y, y+8, y+16, y+24 of word x
-    if (y < 8) {
-      uint32_t c[4] = {0, 0, 0, 0};
-#pragma unroll
-      for (int g = 0; g < MERGE_GROUPS_C; ++g) {
-        const uint32_t v = s_acc[g][y][x];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) c[j] += (v >> (8 * j)) & 0xFFu;
-      }
-      if (wide) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) c[j] += s_wide[x][y + 8 * j];
-      }
-      uint32_t part = 0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) part |= uint32_t(int64_t(c[j]) >= k_min) << (y + 8 * j);
-      s_bits[y][x] = part;
-    }
-    __syncthreads();
-    if (y == 0 && valid) {
-      uint32_t bits = 0;
-#pragma unroll
-      for (int g = 0; g < 8; ++g) bits |= s_bits[g][x];
-      if (L == 1) bits &= 0xFFu;
-      if (leafw) cube[r * OW + (w - leaf_off)] = bits;
-      else pyr[r * PW + w] = bits;
-    }
+  if (wide) {
+    for (int i = y * 32 + x; i < 32 * 33; i += 32 * MERGE_GROUPS_C) (&s_wide[0][0])[i] = 0;
     __syncthreads();
   }
+  uint32_t acc[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q] = 0;
+  int since = 0;
+  if (off >= 0) {
+    uint32_t* p = ws + off;
+    int t = y;
+    for (; t + 3 * MERGE_GROUPS_C < n_groups; t += 4 * MERGE_GROUPS_C) {
+      uint32_t* pa = p + int64_t(t) * stride;
+      const int64_t st = int64_t(MERGE_GROUPS_C) * stride;
+      const uint32_t a = __ldcg(pa), b = __ldcg(pa + st), d = __ldcg(pa + 2 * st), e = __ldcg(pa + 3 * st);
+      if (a) pa[0] = 0u;
+      if (b) pa[st] = 0u;
+      if (d) pa[2 * st] = 0u;
+      if (e) pa[3 * st] = 0u;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        acc[q] += ((a >> q) & 0x01010101u) + ((b >> q) & 0x01010101u) + ((d >> q) & 0x01010101u) +
+                  ((e >> q) & 0x01010101u);
+      since += 4;
+      if (since > 251) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) atomicAdd(&s_wide[x][q + 8 * j], (acc[q] >> (8 * j)) & 0xFFu);
+          acc[q] = 0;
+        }
+        since = 0;
+      }
+    }
+    for (; t < n_groups; t += MERGE_GROUPS_C) {
+      uint32_t* pa = p + int64_t(t) * stride;
+      const uint32_t a = __ldcg(pa);
+      if (a) *pa = 0u;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] += (a >> q) & 0x01010101u;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s_acc[y][q][x] = acc[q];
+  __syncthreads();
+  if (y < 8) {
+    uint32_t c[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int g = 0; g < MERGE_GROUPS_C; ++g) {
+      const uint32_t v = s_acc[g][y][x];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) c[j] += (v >> (8 * j)) & 0xFFu;
+    }
+    if (wide) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) c[j] += s_wide[x][y + 8 * j];
+    }
+    uint32_t part = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) part |= uint32_t(int64_t(c[j]) >= k_min) << (y + 8 * j);
+    s_bits[y][x] = part;
+  }
+  __syncthreads();
+  uint32_t bits = 0;
+  if (y == 0) {
+#pragma unroll
+    for (int g = 0; g < 8; ++g) bits |= s_bits[g][x];
+  }
+  __syncthreads();                     // s_acc / s_bits are reused by the next slot
+  return bits;
 }
 
-// K4: merged path-order pyramid words from the merged cube-order levels
-// (levels < L in `pyr`, level L in the operand).  Eight threads per word,
-// one nibble gather each, OR-combined by shuffles: 8x the threads of a
-// word-per-thread kernel for this latency-bound pass.  Grid (word blocks,
-// regions).
-__global__ void __launch_bounds__(256)
-k_morton_merged(const uint32_t* __restrict__ pyr, const uint32_t* __restrict__ cube, int n_regions, int L,
-                uint32_t* __restrict__ out) {
-  const int64_t PW = pyr_words(L), OW = operand_words(L);
+constexpr int MF_TOP = 2;              // levels 1..MF_TOP (3 words): block 0 of each region
+constexpr int MF_TOP_WORDS = 3;        // pyr_words(2)
+
+// Tile geometry of level l >= 3: words per tile WT = 2^(l-2) (8 rows of 2^l
+// bits), tiles along G' = 2^(l-2); a block holds NWc = max(32, WT) slots.
+__device__ __forceinline__ uint32_t mf_nwc(int l) { return l == 8 ? 64u : 32u; }
+__host__ __device__ __forceinline__ int64_t mf_blocks(int l) {
+  const int64_t n = level_words(l), c = l == 8 ? 64 : 32;
+  return (n + c - 1) / c;
+}
+// cube word of tile t, tile-major slot jj (rows r0 = dr, dg = 0..3; B' fastest)
+__device__ __forceinline__ uint32_t mf_tile_word(int l, uint32_t t, uint32_t jj) {
+  const uint32_t gq_log = uint32_t(l - 2), WT = 1u << (l - 2);
+  const uint32_t rp = t >> gq_log, gq = t & ((1u << gq_log) - 1u);
+  const uint32_t half = WT >> 1;                                    // words per R' value
+  const uint32_t dr = jj / half, q = jj % half;
+  const uint32_t R = 2u * rp + dr;
+  return ((((R << l) + 4u * gq) << l) >> 5) + q;                    // rows (R, 4gq..4gq+3) are contiguous
+}
+
+__global__ void __launch_bounds__(32 * MERGE_GROUPS_C)
+k_merge_fused(uint32_t* __restrict__ ws, int n_groups, int n_regions, int L, int64_t k_min,
+              uint32_t* __restrict__ cube, uint32_t* __restrict__ out) {
+  __shared__ uint32_t s_acc[MERGE_GROUPS_C][8][32];
+  __shared__ uint32_t s_wide[32][33];
+  __shared__ uint32_t s_bits[8][32];
+  __shared__ uint32_t s_m[64];
   const int64_t r = blockIdx.y;
-  const int64_t g = int64_t(blockIdx.x) * 256 + threadIdx.x;
-  const int64_t w = g >> 3;
-  const uint32_t c = uint32_t(g & 7);
-  uint32_t part = 0;
-  if (w < PW) {
-    int l = 1;
-    int64_t off = 0, next = level_words(1);
-    while (l < L && w >= next) { off = next; ++l; next += level_words(l); }
-    const uint32_t* src = (l == L) ? cube + r * OW : pyr + r * PW + off;
-    const uint32_t m = uint32_t(w - off);
-    if (l == 1) {
-      part = c == 0 ? (src[0] & 0xFFu) : 0u;         // cube index == path code at level 1
-    } else {
-      const uint32_t base = code_to_cube(m << 5, l);
-      const uint32_t g0 = c & 1, r0 = (c >> 1) & 1, g1 = (c >> 2) & 1;
-      const uint32_t idx = base + ((g0 | (g1 << 1)) << l) + (r0 << (2 * l));
-      const uint32_t nib = (src[idx >> 5] >> (idx & 31u)) & 0xFu;
-      part = ((nib & 3u) | ((nib & 12u) << 6)) << (g0 * 2 + r0 * 4 + g1 * 16);
+  const int x = threadIdx.x, y = threadIdx.y, tid = y * 32 + x;
+  const int64_t PW = pyr_words(L), CW = cube_words(L), OW = operand_words(L), WSW = ws_words(L);
+  const int64_t stride = WSW * n_regions;
+  const bool wide = (n_groups + MERGE_GROUPS_C - 1) / MERGE_GROUPS_C >= 252;
+  uint32_t* ws_r = ws + r * WSW;
+  uint32_t* cube_r = cube + r * OW;
+  uint32_t* out_r = out + r * PW;
+  if (blockIdx.x == 0) {
+    // levels 1..T (T <= 2): words 0 (level 1), 1..2 (level 2)
+    const int T = L < MF_TOP ? L : MF_TOP;
+    const int nw = int(level_offset(T + 1));
+    const int w = x;
+    int64_t off = -1;
+    const int l = w == 0 ? 1 : 2;
+    if (w < nw) off = (l == L) ? int64_t(w - level_offset(l)) : CW + w;
+    uint32_t bits = merge_slot(ws_r, off, stride, n_groups, k_min, s_acc, s_wide, s_bits, wide);
+    if (y == 0 && w < nw) {
+      if (l == 1) bits &= 0xFFu;
+      s_m[w] = bits;
+      if (l == L) cube_r[w - level_offset(l)] = bits;
+    }
+    __syncthreads();
+    if (tid < nw) {
+      const int lw = tid == 0 ? 1 : 2;
+      const uint32_t m = uint32_t(tid - level_offset(lw));
+      const uint32_t* lv = s_m + level_offset(lw);
+      uint32_t word = 0;
+      const int nb = lw == 1 ? 8 : 32;
+      for (int bb = 0; bb < nb; ++bb) {
+        const uint32_t idx = code_to_cube(m * 32u + uint32_t(bb), lw);
+        word |= ((lv[idx >> 5] >> (idx & 31u)) & 1u) << bb;
+      }
+      out_r[tid] = word;
+    }
+    return;
+  }
+  // tile blocks: level l >= 3
+  int64_t b = int64_t(blockIdx.x) - 1;
+  int l = 3;
+  for (; l <= L; ++l) {
+    const int64_t nb = mf_blocks(l);
+    if (b < nb) break;
+    b -= nb;
+  }
+  if (l > L) return;
+  const uint32_t WT = 1u << (l - 2);                               // words (and path words) per tile
+  const uint32_t NWc = mf_nwc(l);
+  const uint32_t gq_log = uint32_t(l - 2);
+  const uint32_t LW = uint32_t(level_words(l));
+  const uint32_t slot0 = uint32_t(b) * NWc;                        // first tile-major slot of the block
+  const int64_t loff = level_offset(l);
+  for (uint32_t pass = 0; pass < NWc / 32; ++pass) {
+    const uint32_t j = pass * 32 + uint32_t(x);
+    const uint32_t g = slot0 + j;                                  // global tile-major slot
+    int64_t off = -1;
+    uint32_t cw = 0;
+    if (g < LW) {
+      cw = mf_tile_word(l, g / WT, g % WT);
+      off = (l == L) ? int64_t(cw) : CW + loff + cw;
+    }
+    const uint32_t bits = merge_slot(ws_r, off, stride, n_groups, k_min, s_acc, s_wide, s_bits, wide);
+    if (y == 0 && g < LW) {
+      s_m[j] = bits;
+      if (l == L) cube_r[cw] = bits;
     }
   }
-  part |= __shfl_xor_sync(0xFFFFFFFFu, part, 1);
-  part |= __shfl_xor_sync(0xFFFFFFFFu, part, 2);
-  part |= __shfl_xor_sync(0xFFFFFFFFu, part, 4);
-  if (c == 0 && w < PW) out[r * PW + w] = part;
+  __syncthreads();
+  if (uint32_t(tid) < NWc && slot0 + uint32_t(tid) < LW) {
+    // path word: R>>1 = rp, G>>2 = gq, B>>2 = p; bit b0 + 2g0 + 4r0 + 8b1 + 16g1
+    const uint32_t gs = slot0 + uint32_t(tid);
+    const uint32_t t = gs / WT, p = gs % WT;
+    const uint32_t rp = t >> gq_log, gq = t & ((1u << gq_log) - 1u);
+    const uint32_t* tw = s_m + (t * WT - slot0);                    // the tile's words (tile-major)
+    const uint32_t half = WT >> 1;
+    uint32_t word = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t g0 = c & 1, r0 = (c >> 1) & 1, g1 = (c >> 2) & 1;
+      const uint32_t dg = g1 * 2u + g0;
+      // bit of (B' = 4p) in row dg of the R'-half r0: rows are 2^l bits, the
+      // half starts at its first row
+      const uint32_t bit = (dg << l) + 4u * p;
+      const uint32_t wv = tw[r0 * half + (bit >> 5)];
+      const uint32_t nib = (wv >> (bit & 31u)) & 0xFu;
+      word |= ((nib & 3u) | ((nib & 12u) << 6)) << (g0 * 2 + r0 * 4 + g1 * 16);
+    }
+    const uint32_t m = spread3(rp) | (spread3(p) << 1) | (spread3(gq) << 2);
+    out_r[loff + m] = word;
+  }
 }
 
 __global__ void __launch_bounds__(256)
@@ -2076,8 +2155,8 @@ int obg_build_model(const uint8_t* frames, int n_frames, int height, int width, 
   if (levels < 1 || levels > 8) return set_err(OBG_EINVAL, "levels must be in 1..8, got %d", levels);
   if (!tree_pyramids) return set_err(OBG_EINVAL, "null buffer");
   const int64_t n_regions = int64_t(grid_rows) * grid_cols;
-  // K1 + K2c (cube-order levels), K3c (merge; stores every operand word and
-  // zeroes the workspace), K4 (path-order merged pyramid): no memsets at all
+  // K1 (+ cube-order levels), K3f (merge; stores every operand and merged
+  // pyramid word and zeroes the workspace): no memsets at all
   int rc = build_presence_impl(frames, n_frames, height, width, levels, grid_rows, grid_cols, group_size,
                                tree_pyramids, nullptr, workspace, workspace_bytes, flags, nullptr, 0, stream,
                                /*cube_levels=*/true);
@@ -2086,12 +2165,12 @@ int obg_build_model(const uint8_t* frames, int n_frames, int height, int width, 
   const int n_groups = n_frames / group_size;
   const int64_t words = pyr_words(levels) * n_regions;
   if (n_regions > 65535) return set_err(OBG_EUNSUPPORTED, "too many regions (%lld > 65535)", (long long)n_regions);
-  k_merge_cube<<<dim3(unsigned((pyr_words(levels) + 31) / 32), unsigned(n_regions)), dim3(32, MERGE_GROUPS_C), 0, st>>>(
-      tree_pyramids, static_cast<uint32_t*>(workspace), n_groups, int(n_regions), levels, k_min, out_cube);
-  LAUNCH_CHECK("k_merge_cube");
-  k_morton_merged<<<dim3(unsigned((pyr_words(levels) * 8 + 255) / 256), unsigned(n_regions)), 256, 0, st>>>(
-      tree_pyramids, out_cube, int(n_regions), levels, out_merged);
-  LAUNCH_CHECK("k_morton_merged");
+  int64_t blocks = 1;                                   // block 0: levels 1..2
+  for (int l = 3; l <= levels; ++l) blocks += mf_blocks(l);
+  k_merge_fused<<<dim3(unsigned(blocks), unsigned(n_regions)), dim3(32, MERGE_GROUPS_C), 0, st>>>(
+      static_cast<uint32_t*>(workspace), n_groups, int(n_regions), levels, k_min, out_cube, out_merged);
+  LAUNCH_CHECK("k_merge_fused");
+  (void)words;
   return finish_operand(out_cube, n_regions, levels, st);
 }
 

@@ -418,13 +418,14 @@ def test_build_model_groups_and_repeat(cuda):
 
 @pytest.mark.gpu
 def test_build_model_many_trees(cuda):
-    """> 8 x 252 trees per merge: the byte counters of k_merge_cube spill into
-    the 32-bit shared counters (the `wide` path)."""
+    """> 16 x 252 trees per merge: the byte counters of k_merge_fused (16 tree
+    groups) spill into the 32-bit shared counters (the `wide` path); levels 3-7
+    cover its block-0 levels and tile levels."""
     rng = np.random.default_rng(8)
-    n = 2100
+    n = 4100
     base = rng.integers(0, 256, size=(1, 1, 1, 3))
     frames = np.clip(base + rng.integers(-40, 41, size=(n, 8, 16, 3)), 0, 255).astype(np.uint8)
-    for levels, thr in [(4, 0.5), (5, 0.05), (3, 0.99)]:
+    for levels, thr in [(4, 0.5), (5, 0.05), (3, 0.99), (7, 0.02)]:
         cfg = ModelConfig(levels=levels, threshold=thr, training_frames=n)
         model = obg.build_background_model_device(cuda.from_numpy(frames).cuda(), cfg)
         want = orc.build_background_model(list(frames), levels, thr)
