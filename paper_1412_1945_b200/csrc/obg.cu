@@ -702,6 +702,57 @@ __device__ __forceinline__ void build_unit(const uint32_t (&w)[12], uint32_t* bi
 // with atomics).  Cube-order levels are a few instructions per word;
 // path-order ones here cost 5.5x K1's flush (ncu r8), which is why those
 // are made once, for the merged model.  Leaves the bitset zeroed.
+// Levels L-2 .. 1 of a flushed segment by ONE warp, in registers: lane R
+// holds the rows (R, G) of level P = L-1 (2^P bits each); a level is the
+// OR of row pairs (G) and lane pairs (R, one shuffle) with adjacent bit pairs
+// folded (B).  Replaces a chain of four block-wide passes with barriers
+// (~1.5-2k cycles per level, clock64 r3) by ~100 instructions of one warp.
+// Level-l words are OR-ed into `up` (cube-order level_offset layout).
+template <int l, int P>
+__device__ __forceinline__ void warp_levels_down(const uint32_t (&F)[2 << l], uint32_t* up, int lane) {
+  constexpr int M = 1 << l;                        // rows along G (and bits per row) at level l
+  uint32_t Fl[M];
+#pragma unroll
+  for (int g = 0; g < M; ++g) {
+    uint32_t x = F[2 * g] | F[2 * g + 1];
+    x |= __shfl_xor_sync(0xFFFFFFFFu, x, 1 << (P - 1 - l));
+    Fl[g] = fold_pairs(x);                         // 2^l bits
+  }
+  // lanes with R_l = lane >> (P - l) and the low bits clear write row r
+  if ((lane & ((1 << (P - l)) - 1)) == 0 && (lane >> (P - l)) < M) {
+    const uint32_t r = uint32_t(lane >> (P - l));
+    constexpr int RPW = 32 / M < M * M ? 32 / M : M * M;        // rows per word
+    constexpr uint32_t off = uint32_t(level_offset(l));
+#pragma unroll
+    for (int g0 = 0; g0 < M; g0 += RPW) {
+      const uint32_t row0 = r * M + uint32_t(g0);
+      uint32_t w = 0;
+#pragma unroll
+      for (int j = 0; j < RPW && g0 + j < M; ++j) w |= Fl[g0 + j] << (j * M);
+      const uint32_t bit0 = row0 * M;
+      if (w) atomicOr(up + off + (bit0 >> 5), w << (bit0 & 31u));
+    }
+  }
+  if constexpr (l > 1) warp_levels_down<l - 1, P>(Fl, up, lane);
+}
+
+// P = L-1 level words in the flush scratch `lv` (cube order) -> levels P-1..1.
+template <int P>
+__device__ __forceinline__ void warp_upper_levels(const uint32_t* lv, uint32_t* up, int lane) {
+  constexpr int M = 1 << P;
+  uint32_t F[M];
+#pragma unroll
+  for (int g = 0; g < M; ++g) {
+    uint32_t x = 0;
+    if (lane < M) {
+      if constexpr (P == 5) x = lv[lane * 32 + g];                              // one row per word
+      else x = (lv[(lane * M + g) >> 1] >> (16 * (g & 1))) & 0xFFFFu;           // P = 4: two rows per word
+    }
+    F[g] = x;
+  }
+  warp_levels_down<P - 1, P>(F, up, lane);
+}
+
 template <int L, int NT>
 __device__ __forceinline__ void flush_segment(uint32_t* s_bits, uint32_t* dst, int levels_out, bool last) {
   __syncthreads();                                   // the segment's bitset is complete
@@ -721,8 +772,14 @@ __device__ __forceinline__ void flush_segment(uint32_t* s_bits, uint32_t* dst, i
       __syncthreads();
     }
   }
+  // levels L-2..1 (L = 5, 6): warp 0 in registers, while the others start phase B
+  constexpr bool WARP_LEVELS = L == 5 || L == 6;
+  if constexpr (WARP_LEVELS) {
+    if (levels && threadIdx.x < 32)
+      warp_upper_levels<L - 1>(sc + level_offset(L - 1), up, int(threadIdx.x));
+  }
   // phase B: OR the non-zero leaf words into the tree's cube and clear them
-  // (data words only; the pads stay 0), with level L-2 from the scratch
+  // (data words only; the pads stay 0)
   for (uint32_t i = threadIdx.x; i < Smem<L>::data_words; i += NT) {
     const uint32_t p = Smem<L>::data_word(i);
     const uint32_t x = s_bits[p];
@@ -731,7 +788,7 @@ __device__ __forceinline__ void flush_segment(uint32_t* s_bits, uint32_t* dst, i
       if (!last) s_bits[p] = 0u;
     }
   }
-  if constexpr (L >= 3) {
+  if constexpr (L >= 3 && !WARP_LEVELS) {
     if (levels) {
       for (int l = L - 2; l >= 1; --l) {
         const uint32_t nw = uint32_t(level_words(l)), off = uint32_t(level_offset(l));
