@@ -418,7 +418,7 @@ def run_ours(args):
     launches = {("k_build_generic" if not flat else "k_build_l7h" if L == 7 else "k_build_flat"): 1}
     if L >= 7 or not flat:
         launches["k_levels_cube"] = 1
-    launches.update({"k_merge_cube": 1, "k_morton_merged": 1})
+    launches["k_merge_fused"] = 1
     if L == 7:
         launches["k_l7_states"] = 1
     cls_kernel = (f"k_classify_flat<{L}>" if L <= 6 else "k_classify_l7" if L == 7 else "k_classify_flat<8>")
