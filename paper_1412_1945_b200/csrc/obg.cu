@@ -1825,13 +1825,34 @@ __device__ __forceinline__ uint32_t l7_leaf_bit(const uint32_t* __restrict__ cub
   const uint32_t idx = ((x >> 25) << 14) | (((x >> 9) & 127u) << 7) | ((x >> 17) & 127u);
   return (__ldg(cube + (idx >> 5)) >> (idx & 31u)) & 1u;
 }
+// Leaf word of x = [*, G, B, R] rotated so that bit 0 is the pixel's leaf:
+// byte offset R'<<11 | G'<<4 | (B'>>5)<<2 from three shifts and two LOP3s,
+// bit B' & 31 = the low bits of x >> 17 (funnel shifts use them mod 32).
+__device__ __forceinline__ uint32_t l7_leaf_word(const char* __restrict__ cube, uint32_t x) {
+  const uint32_t off = ((x >> 14) & 0x3F800u) | ((x >> 5) & 0x7F0u) | ((x >> 20) & 0xCu);
+  const uint32_t wd = __ldg(reinterpret_cast<const uint32_t*>(cube + off));
+  return __funnelshift_r(wd, wd, x >> 17);
+}
 
+// `leaf_run` (warp-uniform): > 0 while the warp is in leaf mode -- its
+// recent units had pixels in partially filled L6 cells, so the state lookups
+// are skipped and every pixel reads its leaf word directly (~11 instead of
+// ~28 instructions per pixel when every unit is mixed, e.g. a constant-colour
+// scene).  It counts down and the warp retries the state table at 0.
+constexpr int L7_LEAF_RUN = 32;
 template <int OUT>
 __device__ __forceinline__ void classify_unit_l7(const uint32_t (&w)[12], const uint32_t* s_state,
                                                  const uint32_t* __restrict__ cube, uint8_t* mask, int64_t u,
-                                                 ConfAcc& acc) {
+                                                 ConfAcc& acc, int& leaf_run) {
   uint32_t px[16], v[16];
   unpack16<0, 6>(w, px);                                            // [*, G, B, R] operands
+  if (leaf_run > 0) {
+    --leaf_run;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = l7_leaf_word(reinterpret_cast<const char*>(cube), px[j]);
+    emit16<OUT>(v, mask, u, acc);
+    return;
+  }
   uint32_t mixed = 0;
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
@@ -1846,6 +1867,7 @@ __device__ __forceinline__ void classify_unit_l7(const uint32_t (&w)[12], const 
       const uint32_t leaf = l7_leaf_bit(cube, px[j]);
       v[j] = ((v[j] ^ (v[j] >> 1)) & 1u) ? leaf : (v[j] >> 1);
     }
+    leaf_run = L7_LEAF_RUN;
   } else {
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] >>= 1;                        // all children present
@@ -1863,13 +1885,14 @@ k_classify_l7(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_pix
     s_state[(i >> 8) * S7_ROWW + (i & 255u)] = __ldg(cube + cube_words(7) + i);
   __syncthreads();
   const int64_t stride = int64_t(gridDim.x) * S7_BLOCK;
+  int leaf_run = 0;
   for (int64_t u = int64_t(blockIdx.x) * S7_BLOCK + threadIdx.x; u < n_units; u += 2 * stride) {
     const bool second = u + stride < n_units;
     uint32_t wa[12], wb[12];
     load_unit(frames, u, wa);
     if (second) load_unit(frames, u + stride, wb);
-    classify_unit_l7<OUT>(wa, s_state, cube, mask, u, acc);
-    if (second) classify_unit_l7<OUT>(wb, s_state, cube, mask, u + stride, acc);
+    classify_unit_l7<OUT>(wa, s_state, cube, mask, u, acc, leaf_run);
+    if (second) classify_unit_l7<OUT>(wb, s_state, cube, mask, u + stride, acc, leaf_run);
   }
   if constexpr (OUT == OUT_U8 || OUT == OUT_CONF_U8) {
     if (blockIdx.x == 0) {
