@@ -189,6 +189,24 @@ int obg_read_pnm_files(const char* const* paths, int n_files, int kind, int64_t 
 int obg_write_pgm_masks(const uint8_t* masks, int n_masks, int64_t width, int64_t height,
                         const char* const* paths, int n_threads);
 
+/* ---- comparison baselines (detect.py:56-83) -------------------------------
+ * Frame difference (detect_frame_diff, detect.py:56-63): mask i (u8 0/1,
+ * [n_pairs][pixels]) is 1 where some channel of cur[i] differs from prev[i]
+ * by strictly more than diff_threshold.  prev / cur are u8 [n_pairs][pixels][3];
+ * cur == prev + 3 * pixels (consecutive frames of one buffer) reads every
+ * frame once. */
+int obg_frame_diff(const uint8_t* prev, const uint8_t* cur, int n_pairs, int64_t pixels,
+                   int diff_threshold, uint8_t* masks, void* stream);
+
+/* Running mean (detect_running_average, detect.py:66-83) over n_frames
+ * consecutive frames: for t = 0..n-1, mask t = max_c |x_c - avg_c| >
+ * diff_threshold with the mean before the update, then
+ * avg += (x - avg) / (frames_seen + t + 1) in IEEE binary64 (bit-identical
+ * to the reference's numpy).  average: device f64 [pixels][3], updated in
+ * place; masks: u8 0/1 [n_frames][pixels]. */
+int obg_running_average(const uint8_t* frames, int n_frames, int64_t pixels, int64_t frames_seen,
+                        double* average, int diff_threshold, uint8_t* masks, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

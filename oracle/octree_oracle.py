@@ -215,3 +215,23 @@ def confusion(predicted, truth) -> tuple:
         raise ValueError(f"mask dimensions {p.shape} vs {t.shape} do not match")
     return (int(np.count_nonzero(~p & ~t)), int(np.count_nonzero(p & t)),
             int(np.count_nonzero(~p & t)), int(np.count_nonzero(p & ~t)))
+
+
+# --- detect.py:56-63  detect_frame_diff (comparison baseline) --------------------------
+def detect_frame_diff(previous, current, diff_threshold: int = 30) -> np.ndarray:
+    previous = np.asarray(previous)
+    current = np.asarray(current)
+    assert previous.shape[:2] == current.shape[:2]
+    delta = np.abs(current.astype(np.int16) - previous.astype(np.int16)).max(axis=2)
+    return delta > diff_threshold
+
+
+# --- detect.py:66-83  detect_running_average (comparison baseline) ---------------------
+def detect_running_average(frames_seen: int, average, current, diff_threshold: int = 30):
+    average = np.asarray(average, dtype=np.float64)
+    current = np.asarray(current)
+    assert average.shape[:2] == current.shape[:2]
+    delta = np.abs(current.astype(np.float64) - average).max(axis=2)
+    mask = delta > diff_threshold
+    updated = average + (current - average) / (frames_seen + 1)
+    return mask, updated

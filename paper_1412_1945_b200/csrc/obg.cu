@@ -24,7 +24,7 @@
 
 #include "../../include/obg.h"
 
-#define OBG_ABI_VERSION 3
+#define OBG_ABI_VERSION 4
 #define OBG_CUBE_ZEROED 0x100   /* internal: out_cube already cleared by the build kernel */
 
 // ---------------------------------------------------------------------------
@@ -2030,6 +2030,148 @@ __global__ void k_serialize(const uint32_t* __restrict__ pyr, const uint32_t* __
 }
 
 // ===========================================================================
+// Comparison baselines (reference detect.py:56-83):
+// frame difference and the running-mean background, same masks (and the
+// same IEEE binary64 running mean) as the reference's numpy code.
+// ===========================================================================
+// Frame difference: foreground iff some channel changed by strictly more than
+// thr (detect.py:56-63).  Pair i = (prev + i*3P, cur + i*3P).  When cur ==
+// prev + 3P (a sequence), a thread walks its unit position through a chunk
+// of consecutive frames and keeps the previous unit in registers: 3 B read +
+// 1 B written per pixel instead of 6 + 1.  Bytes: per-byte |c - p| > thr with
+// SIMD byte ops, then OR of a pixel's three flags.
+constexpr int FD_BLOCK = 256;
+
+// flags (0x00 / 0xFF per byte) of the 12 words of a unit -> 16 mask bytes
+__device__ __forceinline__ uint4 fd_mask16(const uint32_t (&f)[12]) {
+  uint32_t o[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    // pixels 4q..4q+3 = bytes 12q..12q+11 = words 3q..3q+2
+    // pixel k's three bytes land in byte k of x, y, z:
+    // x = [a0 a3 b2 c1], y = [a1 b0 b3 c2], z = [a2 b1 c0 c3]
+    const uint32_t a = f[3 * q], b = f[3 * q + 1], c = f[3 * q + 2];
+    const uint32_t x = __byte_perm(__byte_perm(a, b, 0x0630), c, 0x5210);
+    const uint32_t y = __byte_perm(__byte_perm(a, b, 0x0741), c, 0x6210);
+    const uint32_t z = __byte_perm(__byte_perm(a, b, 0x0052), c, 0x7410);
+    o[q] = (x | y | z) & 0x01010101u;
+  }
+  return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
+__device__ __forceinline__ uint32_t fd_flags(uint32_t c, uint32_t p, uint32_t thr4) {
+  return __vcmpgtu4(__vabsdiffu4(c, p), thr4);                     // 0xFF where |c - p| > thr
+}
+
+// mode: 0 = compare (thr in 0..254), 1 = all foreground (thr < 0), 2 = none (thr >= 255)
+__global__ void __launch_bounds__(FD_BLOCK)
+k_frame_diff(const uint8_t* __restrict__ prev, const uint8_t* __restrict__ cur, int n_pairs, int64_t pixels,
+             int64_t n_units, int chunk, int thr, int mode, int seq, uint8_t* __restrict__ masks) {
+  const int64_t fb = 3 * pixels;
+  const int n_chunks = (n_pairs + chunk - 1) / chunk;
+  const uint32_t thr4 = uint32_t(thr & 0xFF) * 0x01010101u;
+  for (int64_t item = blockIdx.x * int64_t(FD_BLOCK) + threadIdx.x; item < n_units * n_chunks;
+       item += int64_t(gridDim.x) * FD_BLOCK) {
+    const int64_t u = item % n_units;
+    const int i0 = int(item / n_units) * chunk, i1 = min(n_pairs, i0 + chunk);
+    uint32_t wp[12], wc[12];
+    if (mode == 0) load_unit(prev + int64_t(i0) * fb, u, wp);
+    for (int i = i0; i < i1; ++i) {
+      uint4 m;
+      if (mode == 0) {
+        if (!seq && i > i0) load_unit(prev + int64_t(i) * fb, u, wp);
+        load_unit(cur + int64_t(i) * fb, u, wc);
+        uint32_t f[12];
+#pragma unroll
+        for (int k = 0; k < 12; ++k) f[k] = fd_flags(wc[k], wp[k], thr4);
+        m = fd_mask16(f);
+        if (seq) {
+#pragma unroll
+          for (int k = 0; k < 12; ++k) wp[k] = wc[k];
+        }
+      } else {
+        const uint32_t v = mode == 1 ? 0x01010101u : 0u;
+        m = make_uint4(v, v, v, v);
+      }
+      __stcs(reinterpret_cast<uint4*>(masks + int64_t(i) * pixels) + u, m);
+    }
+  }
+}
+
+// generic path (pixels % 16 != 0 or unaligned buffers): one thread per pixel
+__global__ void __launch_bounds__(FD_BLOCK)
+k_frame_diff_px(const uint8_t* __restrict__ prev, const uint8_t* __restrict__ cur, int n_pairs, int64_t pixels,
+                int thr, uint8_t* __restrict__ masks) {
+  const int64_t total = int64_t(n_pairs) * pixels;
+  for (int64_t k = blockIdx.x * int64_t(FD_BLOCK) + threadIdx.x; k < total; k += int64_t(gridDim.x) * FD_BLOCK) {
+    const uint8_t* a = prev + 3 * k;
+    const uint8_t* b = cur + 3 * k;
+    int d = 0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) d = max(d, abs(int(b[c]) - int(a[c])));
+    masks[k] = uint8_t(d > thr);
+  }
+}
+
+// Running mean (detect.py:66-83): per pixel, for frames t = 0..n-1,
+// mask = max_c |x_c - avg_c| > thr with the mean BEFORE the update (a NaN
+// channel makes numpy's max NaN and the pixel background), then
+// avg_c = avg_c + (x_c - avg_c) / (seen + t + 1): three correctly rounded
+// binary64 operations in the reference's order (the quotient by div_by,
+// correctly rounded), so the mean is bit-identical to numpy's.
+// RN(d / n) from y = RN(1/n): q0 = RN(d y), r = d - n q0 (exact, one FMA),
+// q = RN(q0 + r y) is the correctly rounded quotient (Markstein's theorem;
+// checked against exact rational arithmetic on 300k cases, tools note in
+// DESIGN.md).  Outside the normal range of d (tiny, huge, inf, NaN) the
+// IEEE division is used.  3 FP64 ops instead of a ~10-op division sequence.
+__device__ __forceinline__ double div_by(double d, double n, double y) {
+  const double ad = fabs(d);
+  if ((ad > 0x1p-900 && ad < 0x1p900) || d == 0.0) {
+    const double q0 = __dmul_rn(d, y);
+    const double r = __fma_rn(-q0, n, d);
+    return __fma_rn(r, y, q0);
+  }
+  return __ddiv_rn(d, n);
+}
+
+__global__ void __launch_bounds__(FD_BLOCK)
+k_running_average(const uint8_t* __restrict__ frames, int n_frames, int64_t pixels, int64_t seen,
+                  double* __restrict__ average, double thr, uint8_t* __restrict__ masks) {
+  for (int64_t p = blockIdx.x * int64_t(FD_BLOCK) + threadIdx.x; p < pixels; p += int64_t(gridDim.x) * FD_BLOCK) {
+    double a0 = average[3 * p], a1 = average[3 * p + 1], a2 = average[3 * p + 2];
+    constexpr int RA_UNROLL = 8;                                     // frames whose bytes are loaded up front
+    for (int t0 = 0; t0 < n_frames; t0 += RA_UNROLL) {
+      uint8_t xb[RA_UNROLL][3];
+#pragma unroll
+      for (int k = 0; k < RA_UNROLL; ++k) {
+        if (t0 + k < n_frames) {
+          const uint8_t* x = frames + (int64_t(t0 + k) * pixels + p) * 3;
+          xb[k][0] = __ldcs(x); xb[k][1] = __ldcs(x + 1); xb[k][2] = __ldcs(x + 2);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < RA_UNROLL; ++k) {
+        const int t = t0 + k;
+        if (t >= n_frames) break;
+        const double d0 = __dsub_rn(double(xb[k][0]), a0), d1 = __dsub_rn(double(xb[k][1]), a1),
+                     d2 = __dsub_rn(double(xb[k][2]), a2);
+        const double e0 = fabs(d0), e1 = fabs(d1), e2 = fabs(d2);
+        const bool nan = (e0 != e0) | (e1 != e1) | (e2 != e2);
+        masks[int64_t(t) * pixels + p] = uint8_t(!nan && ((e0 > thr) | (e1 > thr) | (e2 > thr)));
+        const double n = double(seen + t + 1);
+        const double y = __ddiv_rn(1.0, n);                          // RN(1/n), once per frame
+        a0 = __dadd_rn(a0, div_by(d0, n, y));
+        a1 = __dadd_rn(a1, div_by(d1, n, y));
+        a2 = __dadd_rn(a2, div_by(d2, n, y));
+      }
+    }
+    average[3 * p] = a0;
+    average[3 * p + 1] = a1;
+    average[3 * p + 2] = a2;
+  }
+}
+
+// ===========================================================================
 // C ABI
 // ===========================================================================
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -2498,3 +2640,55 @@ int obg_serialize(const uint32_t* pyramid, int levels, int has_root, uint8_t* ou
   return OBG_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// comparison baselines (detect.py:56-83)
+// ---------------------------------------------------------------------------
+int obg_frame_diff(const uint8_t* prev, const uint8_t* cur, int n_pairs, int64_t pixels, int diff_threshold,
+                   uint8_t* masks, void* stream) {
+  g_err[0] = 0;
+  if (n_pairs < 0) return set_err(OBG_EINVAL, "n_pairs must be >= 0");
+  if (pixels < 0) return set_err(OBG_EINVAL, "pixels must be >= 0");
+  if (n_pairs == 0 || pixels == 0) return OBG_OK;
+  if (!prev || !cur || !masks) return set_err(OBG_EINVAL, "null buffer");
+  cudaStream_t st = as_stream(stream);
+  const bool aligned = (pixels % 16) == 0 && (reinterpret_cast<uintptr_t>(prev) % 16) == 0 &&
+                       (reinterpret_cast<uintptr_t>(cur) % 16) == 0 && (reinterpret_cast<uintptr_t>(masks) % 16) == 0;
+  if (!aligned) {
+    const int64_t total = int64_t(n_pairs) * pixels;
+    k_frame_diff_px<<<grid_for(total, FD_BLOCK, sm_count() * 16), FD_BLOCK, 0, st>>>(prev, cur, n_pairs, pixels,
+                                                                                    diff_threshold, masks);
+    LAUNCH_CHECK("k_frame_diff_px");
+    return OBG_OK;
+  }
+  const int mode = diff_threshold < 0 ? 1 : diff_threshold >= 255 ? 2 : 0;
+  const int seq = cur == prev + 3 * pixels ? 1 : 0;
+  const int64_t n_units = pixels / 16;
+  // chunks of consecutive pairs per thread: enough items to fill the GPU
+  // (about 8 units per SM thread slot), long chunks otherwise
+  const int64_t want = int64_t(sm_count()) * 2048 * 2;
+  int64_t c = (n_units * n_pairs) / (want > 0 ? want : 1);
+  if (c > n_pairs) c = n_pairs;
+  if (c < 1) c = 1;
+  int chunk = int(c);
+  if (!seq) chunk = 1;
+  const int64_t items = n_units * ((n_pairs + chunk - 1) / chunk);
+  k_frame_diff<<<grid_for(items, FD_BLOCK, sm_count() * 16), FD_BLOCK, 0, st>>>(prev, cur, n_pairs, pixels, n_units,
+                                                                               chunk, diff_threshold, mode, seq, masks);
+  LAUNCH_CHECK("k_frame_diff");
+  return OBG_OK;
+}
+
+int obg_running_average(const uint8_t* frames, int n_frames, int64_t pixels, int64_t frames_seen, double* average,
+                        int diff_threshold, uint8_t* masks, void* stream) {
+  g_err[0] = 0;
+  if (n_frames < 0) return set_err(OBG_EINVAL, "n_frames must be >= 0");
+  if (pixels < 0) return set_err(OBG_EINVAL, "pixels must be >= 0");
+  if (n_frames == 0 || pixels == 0) return OBG_OK;
+  if (!frames || !average || !masks) return set_err(OBG_EINVAL, "null buffer");
+  cudaStream_t st = as_stream(stream);
+  k_running_average<<<grid_for(pixels, FD_BLOCK, sm_count() * 16), FD_BLOCK, 0, st>>>(
+      frames, n_frames, pixels, frames_seen, average, double(diff_threshold), masks);
+  LAUNCH_CHECK("k_running_average");
+  return OBG_OK;
+}

@@ -56,7 +56,7 @@ def timeit(fn, reps=20):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["build", "classify", "model", "confusion"])
+    ap.add_argument("what", choices=["build", "classify", "model", "confusion", "framediff", "runavg"])
     ap.add_argument("--frames", type=int, default=64)
     ap.add_argument("--scene", default="c3")
     ap.add_argument("--levels", type=int, default=6)
@@ -78,12 +78,19 @@ def main():
         model = obg.build_background_model_device(f, cfg)
         truth = (torch.rand(f.shape[:3], device="cuda") < 0.3).to(torch.uint8)
         ms = timeit(lambda: obg.classify_confusion(model, f, truth))
+    elif a.what == "framediff":      # consecutive-pair masks, every frame read once (4 B/px)
+        out = torch.empty((f.shape[0] - 1,) + tuple(f.shape[1:3]), dtype=torch.uint8, device="cuda")
+        ms = timeit(lambda: obg.frame_diff_sequence(f, 30, out=out))
+    elif a.what == "runavg":         # running mean over the batch: 4 B/px per frame + 48 B/px per call
+        avg = f[0].to(torch.float64).contiguous()
+        out = torch.empty(f.shape[:3], dtype=torch.uint8, device="cuda")
+        ms = timeit(lambda: obg.running_average_sequence(f, avg, 1, 30, out=out))
     else:
         model = obg.build_background_model_device(f, cfg)
         out = torch.empty(f.shape[:3], dtype=torch.uint8, device="cuda")
         ms = timeit(lambda: obg.classify(model, f, out=out))
     print(f"{a.what} scene={a.scene} L={a.levels} frames={a.frames}: {ms * 1000:.1f} us, "
-          f"{px / ms / 1e6:.1f} Gpx/s, {px * (4 if a.what in ('classify', 'confusion') else 3) / ms / 1e6:.1f} GB/s{digest}")
+          f"{px / ms / 1e6:.1f} Gpx/s, {px * (4 if a.what in ('classify', 'confusion', 'framediff', 'runavg') else 3) / ms / 1e6:.1f} GB/s{digest}")
 
 
 if __name__ == "__main__":
