@@ -16,7 +16,9 @@ from .model import BackgroundModel, ModelConfig, build_background_model_device
 
 
 class CapturedStep:
-    """Build-from-``train`` + classify-``test`` as two replayable CUDA graphs."""
+    """Build-from-``train`` + classify-``test`` as replayable CUDA graphs: the
+    two halves separately (build / classify, for per-phase timing) and the
+    whole step as one graph (step)."""
 
     def __init__(self, train, test, config: ModelConfig, packed: bool = False, warmup: int = 2):
         t = _device.torch()
@@ -38,6 +40,12 @@ class CapturedStep:
         self.classify_graph = t.cuda.CUDAGraph()
         with t.cuda.graph(self.classify_graph):
             classify(self.model, test, out=self.masks, packed=packed)
+        # the whole step as ONE graph (no launch gap between build and
+        # classify); it owns its own model buffers, step_model
+        self.step_graph = t.cuda.CUDAGraph()
+        with t.cuda.graph(self.step_graph):
+            self.step_model: BackgroundModel = build_background_model_device(train, config)
+            classify(self.step_model, test, out=self.masks, packed=packed)
         t.cuda.synchronize()
 
     def build(self) -> BackgroundModel:
@@ -49,8 +57,8 @@ class CapturedStep:
         return self.masks
 
     def step(self):
-        self.build_graph.replay()
-        self.classify_graph.replay()
+        """Build + classify, one graph replay; the model is ``step_model``."""
+        self.step_graph.replay()
         return self.masks
 
 
