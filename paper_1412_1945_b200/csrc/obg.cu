@@ -901,9 +901,15 @@ __device__ __forceinline__ void l7h_position(uint32_t x, uint32_t& off, uint32_t
   half = x >> 31;
 }
 
-__device__ __forceinline__ void build_unit_l7h(const uint32_t (&w)[12], uint32_t hpass, bool valid, uint32_t dummy) {
+// Returns nonzero if some pixel of the unit lies in the other half (so the
+// CTA needs its second pass).
+#ifndef OBG_L7_TRACK
+#define OBG_L7_TRACK 2
+#endif
+__device__ __forceinline__ uint32_t build_unit_l7h(const uint32_t (&w)[12], uint32_t hpass, bool valid, uint32_t dummy) {
   uint32_t px[16];
   unpack16<0, 6>(w, px);                                                  // [*, G, B, R] operands
+  uint32_t other = 0;
 #pragma unroll
   for (int g = 0; g < 16; g += 4) {
     uint32_t addr[4], bsel[4], v[4];
@@ -912,6 +918,9 @@ __device__ __forceinline__ void build_unit_l7h(const uint32_t (&w)[12], uint32_t
       uint32_t half;
       l7h_position(px[g + j], addr[j], bsel[j], half);
       const uint32_t wd = lds_at(addr[j]);
+#if OBG_L7_TRACK == 1
+      other |= half ^ hpass;
+#endif
       v[j] = __funnelshift_r(wd, wd, bsel[j]) | (half ^ hpass);            // other half: a hit
     }
     const bool miss = valid && !(v[0] & v[1] & v[2] & v[3] & 1u);
@@ -920,6 +929,16 @@ __device__ __forceinline__ void build_unit_l7h(const uint32_t (&w)[12], uint32_t
       for (int j = 0; j < 4; ++j) reds_or_if(addr[j], 1u << (bsel[j] & 31u), valid ? (v[j] & 1u) : 1u);
     }
   }
+#if OBG_L7_TRACK == 2
+  // R bytes of the 16 pixels sit at bytes 0, 3, 6, 9 of each 12-byte group:
+  // top bits 0x80000080 / 0x00800000 / 0x00008000 of words 3q, 3q+1, 3q+2
+  const uint32_t x0 = hpass ? 0xFFFFFFFFu : 0u;
+  const uint32_t o0 = (w[0] ^ x0) | (w[3] ^ x0) | (w[6] ^ x0) | (w[9] ^ x0);
+  const uint32_t o1 = (w[1] ^ x0) | (w[4] ^ x0) | (w[7] ^ x0) | (w[10] ^ x0);
+  const uint32_t o2 = (w[2] ^ x0) | (w[5] ^ x0) | (w[8] ^ x0) | (w[11] ^ x0);
+  other = (o0 & 0x80000080u) | (o1 & 0x00800000u) | (o2 & 0x00008000u);
+#endif
+  return valid ? other : 0u;
 }
 
 __global__ void __launch_bounds__(L7H_BLOCK, 1)
@@ -941,28 +960,40 @@ k_build_l7h(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t
   const int64_t upt = units_per_frame * group_size;
   const int lane = threadIdx.x & 31;
   const uint32_t dummy = 4u * (L7H_WORDS + uint32_t(lane));
-  for (uint32_t h = 0; h < 2; ++h) {
+  // First pass: the half of the range's first pixel (R' top bit = R >> 7);
+  // the second pass only if the first one met a pixel of the other half
+  // (a constant or dark scene needs one read of its frames, not two).
+  const uint32_t h_first = uint32_t(__ldg(frames + 48 * u_begin)) >> 7;
+  uint32_t need_other = 0;
+  for (uint32_t pass = 0; pass < 2; ++pass) {
+#if OBG_L7_TRACK == 0
+    need_other = 1;
+#endif
+    if (pass == 1 && !__syncthreads_or(int(need_other))) break;
+    const uint32_t h = pass == 0 ? h_first : 1u - h_first;
     int64_t u = u_begin;
     while (u < u_end) {
       const int64_t tree = u / upt;
       const int64_t seg_end = min(u_end, (tree + 1) * upt);
-      int64_t wv = u + threadIdx.x - lane;
+      // 32-bit trip counts and a pointer bump per iteration (as k_build_flat)
+      const int64_t seg_len = seg_end - u;
+      const int32_t rel0 = int32_t(threadIdx.x) - lane;
+      const int32_t n_it = seg_len > rel0 ? int32_t((seg_len - rel0 + L7H_BLOCK - 1) / L7H_BLOCK) : 0;
+      const int32_t n_lane =
+          seg_len > rel0 + lane ? int32_t((seg_len - rel0 - lane + L7H_BLOCK - 1) / L7H_BLOCK) : 0;
+      constexpr int64_t STEP = 48 * int64_t(L7H_BLOCK);
+      const uint8_t* fp = frames + 48 * (u + rel0 + lane);
       uint32_t wa[12], wb[12];
-      if (wv + lane < seg_end) load_unit(frames, wv + lane, wa);
-      while (wv < seg_end) {
-        {
-          const int64_t wn = wv + L7H_BLOCK;
-          if (wn + lane < seg_end) load_unit(frames, wn + lane, wb);
-          build_unit_l7h(wa, h, wv + lane < seg_end, dummy);
-          wv = wn;
-        }
-        if (wv >= seg_end) break;
-        {
-          const int64_t wn = wv + L7H_BLOCK;
-          if (wn + lane < seg_end) load_unit(frames, wn + lane, wa);
-          build_unit_l7h(wb, h, wv + lane < seg_end, dummy);
-          wv = wn;
-        }
+      if (0 < n_lane) load_unit_at(fp, wa);
+      for (int32_t k = 0; k < n_it;) {
+        if (k + 1 < n_lane) load_unit_at(fp + STEP, wb);
+        need_other |= build_unit_l7h(wa, h, k < n_lane, dummy);
+        fp += STEP;
+        if (++k >= n_it) break;
+        if (k + 1 < n_lane) load_unit_at(fp + STEP, wa);
+        need_other |= build_unit_l7h(wb, h, k < n_lane, dummy);
+        fp += STEP;
+        ++k;
       }
       // flush this half of the tree's leaf cube, leave the half-cube zeroed
       __syncthreads();
@@ -1807,7 +1838,13 @@ k_classify_flat(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_p
 // State word (R6, G6, B6/16) = SWAR over the 4 cube words of rows
 // (2R6+{0,1}, 2G6+{0,1}): bit pairs (2b, 2b+1) are the children along B'.
 // ---------------------------------------------------------------------------
-constexpr int S7_BLOCK = 256;
+#ifndef OBG_S7_BLOCK
+#define OBG_S7_BLOCK 512        // 2 CTAs per SM (66 KB state table each): 1024 threads, -12 % at uniform L7
+#endif
+#ifndef OBG_S7_MINB
+#define OBG_S7_MINB 2
+#endif
+constexpr int S7_BLOCK = OBG_S7_BLOCK;
 constexpr uint32_t S7_ROWW = 257;                          // 64 G6 x 4 words + pad
 constexpr uint32_t S7_WORDS = 64 * S7_ROWW;
 
@@ -1876,7 +1913,7 @@ __device__ __forceinline__ void classify_unit_l7(const uint32_t (&w)[12], const 
 }
 
 template <int OUT>
-__global__ void __launch_bounds__(S7_BLOCK, 3)
+__global__ void __launch_bounds__(S7_BLOCK, OBG_S7_MINB)
 k_classify_l7(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_pixels, const uint32_t* __restrict__ cube,
               uint8_t* __restrict__ mask, unsigned long long* counts) {
   ConfAcc acc;
@@ -2261,6 +2298,8 @@ static int launch_build_l7h(const uint8_t* frames, int64_t units_per_frame, int6
   int64_t per_cta = (total_units + max_ctas - 1) / max_ctas;
   const int64_t min_per_cta = int64_t(L7H_BLOCK) * 4;
   if (per_cta < min_per_cta) per_cta = min_per_cta;
+  if (per_cta >= (int64_t(1) << 31) - 2 * L7H_BLOCK)
+    return set_err(OBG_EUNSUPPORTED, "too many pixels per launch (%lld units per CTA)", (long long)per_cta);
   const int grid = int((total_units + per_cta - 1) / per_cta);
   k_build_l7h<<<grid, L7H_BLOCK, smem, st>>>(frames, units_per_frame, total_units, group_size, per_cta, ws, out_pyr,
                                              n_trees, zero_cube, zero_words);

@@ -36,10 +36,10 @@ class CapturedStep:
         t.cuda.synchronize()
         self.build_graph = t.cuda.CUDAGraph()
         with t.cuda.graph(self.build_graph):
-            self.model: BackgroundModel = build_background_model_device(train, config)
+            self.build_model: BackgroundModel = build_background_model_device(train, config)
         self.classify_graph = t.cuda.CUDAGraph()
         with t.cuda.graph(self.classify_graph):
-            classify(self.model, test, out=self.masks, packed=packed)
+            classify(self.build_model, test, out=self.masks, packed=packed)
         # the whole step as ONE graph (no launch gap between build and
         # classify); it owns its own model buffers, step_model
         self.step_graph = t.cuda.CUDAGraph()
@@ -47,18 +47,27 @@ class CapturedStep:
             self.step_model: BackgroundModel = build_background_model_device(train, config)
             classify(self.step_model, test, out=self.masks, packed=packed)
         t.cuda.synchronize()
+        self._last = self.build_model
+
+    @property
+    def model(self) -> BackgroundModel:
+        """The model of the most recent replay (build() or step())."""
+        return self._last
 
     def build(self) -> BackgroundModel:
         self.build_graph.replay()
-        return self.model
+        self._last = self.build_model
+        return self.build_model
 
     def classify(self):
+        """Classify with the model of the last build()."""
         self.classify_graph.replay()
         return self.masks
 
     def step(self):
-        """Build + classify, one graph replay; the model is ``step_model``."""
+        """Build + classify as one graph replay (model: ``self.model``)."""
         self.step_graph.replay()
+        self._last = self.step_model
         return self.masks
 
 

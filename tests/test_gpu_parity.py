@@ -340,9 +340,13 @@ def test_captured_step_matches_eager(cuda, golden):
         step.model._trees = None        # re-materialise from the device after the next replay
         for i in range(len(masks)):
             assert mask_digest(masks[i]) == rec["mask_sha"][i]
-    # new frames copied into the static input: the replay classifies them
+    # new frames copied into the static input: the replays classify them --
+    # the one-graph step and the split build / classify graphs alike
     test.copy_(cuda.from_numpy(sc.train[:24]).cuda())
     eager = obg.classify(step.model, test).clone()
+    assert cuda.equal(step.step(), eager)
+    step.build()
+    assert sha(step.model.trees[0][0].to_bytes()) == rec["merged_sha"]
     assert cuda.equal(step.classify(), eager)
     want = orc.build_background_model(list(sc.train), rec["levels"], rec["threshold"])
     for i in range(0, 24, 6):
