@@ -877,6 +877,155 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
 }
 
 // ---------------------------------------------------------------------------
+// K1 for L = 5 (and 4) with a BYTE per leaf (32 / 4 KB table): a pixel's leaf
+// is recorded with one plain byte store of 1 -- idempotent, so no lookup,
+// no warp vote, no miss path and no atomics (the bit-per-leaf K1 spends
+// ~8 instructions per pixel on lookup + test + vote, and its miss path on
+// every first sighting).  Row layout: byte R' * RS + G' * 2^L + B', rows of
+// RS = 4^L + 16 bytes (16-byte aligned; 4 pad words skew R' across banks).
+// At a tree boundary the table is packed into the bit-per-leaf row layout
+// (Smem<L>, right after the table) and flushed by flush_segment as before.
+// ---------------------------------------------------------------------------
+template <int L>
+struct ByteTab {
+  static constexpr int s = 8 - L;
+  static constexpr uint32_t RS = (1u << (2 * L)) + 16u;          // bytes per R' row
+  static constexpr uint32_t BYTES = (1u << L) * RS;
+  static constexpr uint32_t BITS_OFF = (BYTES + 1023u) & ~1023u;  // byte offset of the Smem<L> bitset
+  static_assert(RS % (1u << s) == 0 && RS % 16 == 0, "row stride");
+};
+
+// byte offsets of pixels 2K and 2K+1 of a unit in the table
+template <int L, int K>
+__device__ __forceinline__ void byte_pair(const uint32_t (&w)[12], uint32_t& a, uint32_t& b) {
+  using T = ByteTab<L>;
+  constexpr int s = T::s;
+  constexpr uint32_t M = (1u << L) - 1u;
+  constexpr int o = 6 * K, i = o >> 2, j = o & 3;
+  constexpr uint32_t selR = uint32_t(j) | (uint32_t(j) << 4) | (uint32_t(j + 3) << 8) | (uint32_t(j + 3) << 12);
+  constexpr uint32_t selG = uint32_t(j + 1) | (uint32_t(j + 2) << 4) | (uint32_t(j + 4) << 8) | (uint32_t(j + 5) << 12);
+  const uint32_t yR = __byte_perm(w[i], w[i + 1], selR);           // [R_A, R_A, R_B, R_B]
+  const uint32_t yG = __byte_perm(w[i], w[i + 1], selG);           // [G_A, B_A, G_B, B_B]
+  const uint32_t P = yR & ((M << s) | (M << (s + 16)));            // R & ~(2^s-1) per half
+  const uint32_t gq = yG & ((M << s) | (M << (s + 16)));           // G & ~(2^s-1): G' << s
+  const uint32_t bq = (yG >> (8 + s)) & (M | (M << 16));           // B'
+  uint32_t q;
+  if constexpr (2 * L - 8 >= 0) q = (gq << (2 * L - 8)) | bq;      // G' << L | B'
+  else q = (gq >> (8 - 2 * L)) | bq;
+  const uint32_t pair = P * (T::RS >> s) + q;
+  b = __umulhi(pair, 1u << 16);
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(a) : "r"(b), "r"(0xFFFF0000u), "r"(pair));   // pair & 0xFFFF
+}
+
+__device__ __forceinline__ void sts_one(uint32_t off) {
+  asm volatile("st.shared.u8 [%0+1024], %1;" :: "r"(off), "r"(1u) : "memory");
+}
+
+template <int L, bool FULL>
+__device__ __forceinline__ void build_unit_bytes(const uint32_t (&w)[12], bool valid) {
+  // lanes past the segment store nothing (a warp-uniform branch in the
+  // steady state, FULL)
+  if (!FULL && !valid) return;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    uint32_t a, b;
+    switch (k) {
+      case 0: byte_pair<L, 0>(w, a, b); break;
+      case 1: byte_pair<L, 1>(w, a, b); break;
+      case 2: byte_pair<L, 2>(w, a, b); break;
+      case 3: byte_pair<L, 3>(w, a, b); break;
+      case 4: byte_pair<L, 4>(w, a, b); break;
+      case 5: byte_pair<L, 5>(w, a, b); break;
+      case 6: byte_pair<L, 6>(w, a, b); break;
+      default: byte_pair<L, 7>(w, a, b); break;
+    }
+    sts_one(a);
+    sts_one(b);
+  }
+}
+
+// 4 bytes of 0/1 -> 4 bits
+__device__ __forceinline__ uint32_t pack4(uint32_t x) { return (x * 0x10204080u) >> 28; }
+
+// Pack the byte table into the Smem<L> bit-per-leaf rows (and clear it).
+template <int L>
+__device__ __forceinline__ void pack_byte_table(uint32_t* s_tab, uint32_t* s_bits, bool clear) {
+  using T = ByteTab<L>;
+  using S = Smem<L>;
+  constexpr uint32_t ROWS = 1u << (2 * L);                         // (R', G') rows of 2^L bytes
+  for (uint32_t r = threadIdx.x; r < ROWS; r += BUILD_BLOCK) {
+    const uint32_t R = r >> L, G = r & ((1u << L) - 1u);
+    uint4* src = reinterpret_cast<uint4*>(reinterpret_cast<char*>(s_tab) + R * T::RS + (G << L));
+    uint32_t bits = 0;
+#pragma unroll
+    for (int v = 0; v < (1 << L) / 16; ++v) {
+      const uint4 q = src[v];
+      bits |= (pack4(q.x) | (pack4(q.y) << 4) | (pack4(q.z) << 8) | (pack4(q.w) << 12)) << (16 * v);
+      if (clear) src[v] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    if constexpr (L == 5) s_bits[R * S::ROWW + G] = bits;
+    else s_bits[R * S::ROWW + G] = bits * S::REP;                  // L = 4: 16-bit row replicated
+  }
+}
+
+template <int L>
+__global__ void __launch_bounds__(BUILD_BLOCK, OBG_BUILD_MINB)
+k_build_bytes(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t total_units,
+              int group_size, int64_t units_per_cta, uint32_t* __restrict__ ws,
+              uint32_t* __restrict__ out_pyr, int64_t n_trees, uint32_t* __restrict__ zero_cube,
+              int64_t zero_words, int levels_out) {
+  using T = ByteTab<L>;
+  extern __shared__ __align__(1024) uint32_t s_tab[];
+  if (static_cast<uint32_t>(__cvta_generic_to_shared(s_tab)) != DYN_SMEM_BASE) __trap();
+  uint32_t* s_bits = s_tab + T::BITS_OFF / 4;
+  constexpr int64_t WSW = ws_words(L);
+  if (blockIdx.x == 0) {
+    clear_shared_words(out_pyr, n_trees, L);
+    for (int64_t i = threadIdx.x; i < zero_words; i += BUILD_BLOCK) zero_cube[i] = 0u;
+  }
+  const int64_t u_begin = int64_t(blockIdx.x) * units_per_cta;
+  const int64_t u_end = min(total_units, u_begin + units_per_cta);
+  if (u_begin >= u_end) return;
+  for (uint32_t i = threadIdx.x; i < T::BYTES / 16; i += BUILD_BLOCK)
+    reinterpret_cast<uint4*>(s_tab)[i] = make_uint4(0u, 0u, 0u, 0u);
+  for (uint32_t i = threadIdx.x; i < Smem<L>::compact; i += BUILD_BLOCK) s_bits[Smem<L>::compact_word(i)] = 0u;
+  __syncthreads();
+  const int64_t units_per_tree = units_per_frame * group_size;
+  int64_t u = u_begin;
+  while (u < u_end) {
+    const int64_t tree = u / units_per_tree;
+    const int64_t seg_end = min(u_end, (tree + 1) * units_per_tree);
+    const int lane = threadIdx.x & 31;
+    const int64_t seg_len = seg_end - u;
+    const int32_t rel0 = int32_t(threadIdx.x) - lane;
+    const int32_t n_it = seg_len > rel0 ? int32_t((seg_len - rel0 + BUILD_BLOCK - 1) / BUILD_BLOCK) : 0;
+    const int32_t n_full = seg_len >= rel0 + 32 ? int32_t((seg_len - rel0 - 32) / BUILD_BLOCK) + 1 : 0;
+    const int32_t n_lane = seg_len > rel0 + lane ? int32_t((seg_len - rel0 - lane + BUILD_BLOCK - 1) / BUILD_BLOCK) : 0;
+    constexpr int64_t STEP = 48 * int64_t(BUILD_BLOCK);
+    const uint8_t* fp = frames + 48 * (u + rel0 + lane);
+    uint32_t wa[12], wb[12];
+    if (0 < n_lane) load_unit_at(fp, wa);
+    for (int32_t k = 0; k < n_it;) {
+      if (k + 1 < n_lane) load_unit_at(fp + STEP, wb);
+      if (k < n_full) build_unit_bytes<L, true>(wa, true);
+      else build_unit_bytes<L, false>(wa, k < n_lane);
+      fp += STEP;
+      if (++k >= n_it) break;
+      if (k + 1 < n_lane) load_unit_at(fp + STEP, wa);
+      if (k < n_full) build_unit_bytes<L, true>(wb, true);
+      else build_unit_bytes<L, false>(wb, k < n_lane);
+      fp += STEP;
+      ++k;
+    }
+    const bool last = seg_end >= u_end;
+    __syncthreads();                                  // the segment's table is complete
+    pack_byte_table<L>(s_tab, s_bits, !last);
+    flush_segment<L, BUILD_BLOCK>(s_bits, ws + tree * WSW, levels_out, last);
+    u = seg_end;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K1, L = 7: the 2^21-bit leaf set (256 KB) does not fit shared memory, so
 // the CTA streams its range twice, once per half of the cube (R' top bit h),
 // with that half (128 KB, skewed rows: R' & 63 x 128 G' x 4 B' words + pad)
@@ -2247,6 +2396,9 @@ int obg_pack_codes(const uint8_t* pixels, int64_t n_pixels, int levels, uint32_t
   return OBG_OK;
 }
 
+#ifndef OBG_BYTE_TABLE
+#define OBG_BYTE_TABLE 1
+#endif
 template <int L>
 static int launch_build_flat(const uint8_t* frames, int64_t units_per_frame, int64_t total_units, int group_size,
                              uint32_t* ws, uint32_t* out_pyr, int64_t n_trees, uint32_t* zero_cube, int64_t zero_words,
@@ -2275,6 +2427,25 @@ static int launch_build_flat(const uint8_t* frames, int64_t units_per_frame, int
   if (per_cta >= (int64_t(1) << 31) - 2 * BUILD_BLOCK)
     return set_err(OBG_EUNSUPPORTED, "too many pixels per launch (%lld units per CTA)", (long long)per_cta);
   const int grid = int((total_units + per_cta - 1) / per_cta);
+#if OBG_BYTE_TABLE
+  // L = 5 only: at L = 4 uniform-random frames lose more to bank conflicts
+  // of the scattered byte stores than the lookups cost (A/B: L5 -2..-5 %,
+  // L4 uniform +5 %)
+  if constexpr (L == 5) {
+    if (!counts) {
+      const size_t smem_b = ByteTab<L>::BITS_OFF + size_t(Smem<L>::alloc_words) * 4;
+      static bool attr = false;
+      if (!attr) {
+        CUDA_TRY(cudaFuncSetAttribute(k_build_bytes<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_b)));
+        attr = true;
+      }
+      k_build_bytes<L><<<grid, BUILD_BLOCK, smem_b, st>>>(frames, units_per_frame, total_units, group_size, per_cta,
+                                                          ws, out_pyr, n_trees, zero_cube, zero_words, levels_out);
+      LAUNCH_CHECK("k_build_bytes");
+      return OBG_OK;
+    }
+  }
+#endif
   if (counts)
     k_build_flat<L, SMEM, true><<<grid, BUILD_BLOCK, smem, st>>>(frames, units_per_frame, total_units, group_size,
                                                                  per_cta, ws, out_pyr, n_trees, zero_cube, zero_words, counts, levels_out);
