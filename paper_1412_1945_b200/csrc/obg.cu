@@ -208,7 +208,7 @@ struct SmemT {
   // index i -> word compact_word(i))
   static constexpr int64_t words = split ? HALF + ROWS : skew ? ROWS : cube_words(L);
   static constexpr uint32_t compact = split ? 2u * ROWS : uint32_t(words);
-  // first of 32 per-lane dummy words (build kernel atomics that must not land)
+  // 32 spare words (formerly per-lane dummy atomic targets; the layout keeps them)
   static constexpr uint32_t DUMMY = split ? ROWS : uint32_t(words);
   // build kernel: cube-order levels 1..L-1 of a flushed segment (level_offset
   // layout); in the hole when split
@@ -343,15 +343,12 @@ __device__ __forceinline__ uint32_t rgb_word_scalar(const uint8_t* p) {
 // (and those of a second unit) issued back to back: left to itself ptxas sinks
 // them next to their first use to save registers, which starves the memory
 // pipe (ncu r2: long-scoreboard stalls dominated classify).
-#ifndef OBG_LD_HINT
-#define OBG_LD_HINT ""
-#endif
 __device__ __forceinline__ void load_unit_at(const uint8_t* p, uint32_t (&w)[12]) {
-  asm volatile("ld.global.nc" OBG_LD_HINT ".v4.u32 {%0, %1, %2, %3}, [%4];"
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
                : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "l"(p));
-  asm volatile("ld.global.nc" OBG_LD_HINT ".v4.u32 {%0, %1, %2, %3}, [%4+16];"
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4+16];"
                : "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]) : "l"(p));
-  asm volatile("ld.global.nc" OBG_LD_HINT ".v4.u32 {%0, %1, %2, %3}, [%4+32];"
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4+32];"
                : "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]) : "l"(p));
 }
 __device__ __forceinline__ void load_unit(const uint8_t* __restrict__ base, int64_t u, uint32_t (&w)[12]) {
@@ -640,7 +637,7 @@ __device__ __forceinline__ bool all_hit4(const uint32_t (&v)[4]) {
 // pixels miss at C3 (first occurrences of a colour within a CTA's range).
 template <int L, bool SMEM_BITS, bool COUNTS, bool FULL>
 __device__ __forceinline__ void build_unit(const uint32_t (&w)[12], uint32_t* bits, uint32_t* cnt,
-                                           bool valid_, uint32_t dummy) {
+                                           bool valid_) {
   // FULL: every lane of the warp holds a unit (the steady state); the tail
   // variant carries per-lane `valid`
   const bool valid = FULL || valid_;
@@ -846,7 +843,6 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
     // 32-bit trip counts and a pointer bump per iteration: the 64-bit unit
     // indices cost ~1.2 instructions per pixel (ncu r18).
     const int lane = threadIdx.x & 31;
-    const uint32_t dummy = 4u * (Smem<L>::DUMMY + uint32_t(lane));   // byte offset
     const int64_t seg_len = seg_end - u;                               // < 2^31 (host checks units_per_cta)
     const int32_t rel0 = int32_t(threadIdx.x) - lane;                  // warp's first unit
     const int32_t n_it = seg_len > rel0 ? int32_t((seg_len - rel0 + BUILD_BLOCK - 1) / BUILD_BLOCK) : 0;
@@ -857,8 +853,8 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
 #define OBG_BUILD_STEP(CUR, NXT)                                                              \
     {                                                                                          \
       if (k + STAGES - 1 < n_lane) load_unit_at(fp + (STAGES - 1) * STEP, NXT);                \
-      if (k < n_full) build_unit<L, SMEM_BITS, COUNTS, true>(CUR, bits, cnt, true, dummy);     \
-      else build_unit<L, SMEM_BITS, COUNTS, false>(CUR, bits, cnt, k < n_lane, dummy);         \
+      if (k < n_full) build_unit<L, SMEM_BITS, COUNTS, true>(CUR, bits, cnt, true);            \
+      else build_unit<L, SMEM_BITS, COUNTS, false>(CUR, bits, cnt, k < n_lane);                \
       fp += STEP;                                                                              \
       ++k;                                                                                     \
     }
@@ -1055,7 +1051,7 @@ __device__ __forceinline__ void l7h_position(uint32_t x, uint32_t& off, uint32_t
 #ifndef OBG_L7_TRACK
 #define OBG_L7_TRACK 2
 #endif
-__device__ __forceinline__ uint32_t build_unit_l7h(const uint32_t (&w)[12], uint32_t hpass, bool valid, uint32_t dummy) {
+__device__ __forceinline__ uint32_t build_unit_l7h(const uint32_t (&w)[12], uint32_t hpass, bool valid) {
   uint32_t px[16];
   unpack16<0, 6>(w, px);                                                  // [*, G, B, R] operands
   uint32_t other = 0;
@@ -1108,7 +1104,6 @@ k_build_l7h(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t
   __syncthreads();
   const int64_t upt = units_per_frame * group_size;
   const int lane = threadIdx.x & 31;
-  const uint32_t dummy = 4u * (L7H_WORDS + uint32_t(lane));
   // First pass: the half of the range's first pixel (R' top bit = R >> 7);
   // the second pass only if the first one met a pixel of the other half
   // (a constant or dark scene needs one read of its frames, not two).
@@ -1136,11 +1131,11 @@ k_build_l7h(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t
       if (0 < n_lane) load_unit_at(fp, wa);
       for (int32_t k = 0; k < n_it;) {
         if (k + 1 < n_lane) load_unit_at(fp + STEP, wb);
-        need_other |= build_unit_l7h(wa, h, k < n_lane, dummy);
+        need_other |= build_unit_l7h(wa, h, k < n_lane);
         fp += STEP;
         if (++k >= n_it) break;
         if (k + 1 < n_lane) load_unit_at(fp + STEP, wa);
-        need_other |= build_unit_l7h(wb, h, k < n_lane, dummy);
+        need_other |= build_unit_l7h(wb, h, k < n_lane);
         fp += STEP;
         ++k;
       }
