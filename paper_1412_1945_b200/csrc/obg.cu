@@ -2021,6 +2021,16 @@ __device__ __forceinline__ uint32_t l7_leaf_word(const char* __restrict__ cube, 
 // ~28 instructions per pixel when every unit is mixed, e.g. a constant-colour
 // scene).  It counts down and the warp retries the state table at 0.
 constexpr int L7_LEAF_RUN = 32;
+constexpr int L7_LEAF_LANES = 4;       // A/B: 4 lanes keeps C3-like scenes at L7 in leaf mode, uniform 2.7x faster
+
+// l7_leaf_word, the load predicated on `pred` (0 without a memory access)
+__device__ __forceinline__ uint32_t l7_leaf_word_if(const char* __restrict__ cube, uint32_t x, uint32_t pred) {
+  const uint32_t off = ((x >> 14) & 0x3F800u) | ((x >> 5) & 0x7F0u) | ((x >> 20) & 0xCu);
+  uint32_t wd = 0;
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.global.nc.u32 %0, [%1];\n\t}"
+               : "+r"(wd) : "l"(cube + off), "r"(pred));
+  return __funnelshift_r(wd, wd, x >> 17);
+}
 template <int OUT>
 __device__ __forceinline__ void classify_unit_l7(const uint32_t (&w)[12], const uint32_t* s_state,
                                                  const uint32_t* __restrict__ cube, uint8_t* mask, int64_t u,
@@ -2040,15 +2050,19 @@ __device__ __forceinline__ void classify_unit_l7(const uint32_t (&w)[12], const 
     v[j] = s7_state(s_state, px[j]);
     mixed |= (v[j] ^ (v[j] >> 1)) & 1u;                             // some but not all leaves
   }
-  if (__any_sync(__activemask(), mixed)) {
-    // branch-free: every pixel of the unit reads its leaf bit (L1-resident
-    // when the cells are few), partial cells take it
+  const uint32_t bal = __ballot_sync(__activemask(), mixed);
+  if (bal) {
+    // branch-free: pixels in partially filled cells read their leaf word
+    // (predicated loads: no traffic for the others)
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const uint32_t leaf = l7_leaf_bit(cube, px[j]);
-      v[j] = ((v[j] ^ (v[j] >> 1)) & 1u) ? leaf : (v[j] >> 1);
+      const uint32_t mj = (v[j] ^ (v[j] >> 1)) & 1u;
+      v[j] = mj ? l7_leaf_word_if(reinterpret_cast<const char*>(cube), px[j], mj) : (v[j] >> 1);
     }
-    leaf_run = L7_LEAF_RUN;
+    // leaf mode only where partial cells are common (several lanes met one):
+    // with sparse partial cells (e.g. uniform-random frames and a nearly
+    // full model) the state table answers almost every pixel
+    if (__popc(bal) >= L7_LEAF_LANES) leaf_run = L7_LEAF_RUN;
   } else {
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] >>= 1;                        // all children present
