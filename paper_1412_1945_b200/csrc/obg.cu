@@ -873,6 +873,149 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
 }
 
 // ---------------------------------------------------------------------------
+// K1 with a region grid (R x C > 1, model.py:61-75, 93-109), L <= 6,
+// W % 16 == 0: blockIdx.y = region row r (a band of rows); the CTA keeps one
+// shared bitset per column region (C of them, BB bytes apart) and streams
+// the band's units; at a tree (frame group) boundary it flushes bitset c into
+// tree g * R * C + r * C + c.  A unit cut by a column boundary is handled per
+// pixel by its lanes after the warp's vote-based pass (where they count as
+// invalid), so warp collectives stay converged.
+// ---------------------------------------------------------------------------
+template <int L>
+struct BandBits {
+  static constexpr uint32_t ALLOC = (uint32_t(Smem<L>::alloc_words) + 31u) & ~31u;   // words per bitset
+};
+
+template <int L>
+__device__ __forceinline__ void build_unit_band(const uint32_t (&w)[12], bool valid, uint32_t ob) {
+#pragma unroll
+  for (int g = 0; g < 16; g += 4) {
+    uint32_t addr[4], bsel[4], v[4];
+    pair_positions_dyn<Smem<L>>(w, g / 2, 0u, addr[0], bsel[0], addr[1], bsel[1]);
+    pair_positions_dyn<Smem<L>>(w, g / 2 + 1, 0u, addr[2], bsel[2], addr[3], bsel[3]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      addr[j] += ob;
+      const uint32_t wd = lds_at(addr[j]);
+      v[j] = __funnelshift_r(wd, wd, bsel[j]);
+    }
+    const bool miss = valid && !all_hit4(v);
+    if (__any_sync(0xFFFFFFFFu, miss)) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) reds_or_if(addr[j], Smem<L>::set_mask(bsel[j]), valid ? (v[j] & 1u) : 1u);
+    }
+  }
+}
+
+// per pixel (a unit cut by a column boundary): pixel j at column x0 + j
+template <int L>
+__device__ __forceinline__ void build_unit_band_px(const uint32_t (&w)[12], int x0, const int* cb, int C) {
+  uint32_t px[16];
+  unpack16<0, L>(w, px);
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    int c = 0;
+    while (c + 1 < C && x0 + j >= cb[c + 1]) ++c;
+    uint32_t addr, bsel;
+    bit_position<L, Smem<L>>(px[j], addr, bsel);
+    addr += uint32_t(c) * (BandBits<L>::ALLOC * 4u);
+    const uint32_t wd = lds_at(addr);
+    reds_or_if(addr, Smem<L>::set_mask(bsel), __funnelshift_r(wd, wd, bsel) & 1u);
+  }
+}
+
+template <int L>
+__global__ void __launch_bounds__(BUILD_BLOCK, 1)
+k_build_band(const uint8_t* __restrict__ frames, int n_frames_used, int H, int W, int R, int C, int group_size,
+             int64_t per_cta, uint32_t* __restrict__ ws, uint32_t* __restrict__ out_pyr, int64_t n_trees,
+             uint32_t* __restrict__ zero_cube, int64_t zero_words, int levels_out) {
+  constexpr uint32_t ALLOC = BandBits<L>::ALLOC;
+  constexpr int64_t WSW = ws_words(L);
+  // dynamic smem only (the bitsets must start at DYN_SMEM_BASE): C bitsets,
+  // then the C + 1 column boundaries
+  extern __shared__ __align__(1024) uint32_t s_bits[];
+  if (static_cast<uint32_t>(__cvta_generic_to_shared(s_bits)) != DYN_SMEM_BASE) __trap();
+  int* s_cb = reinterpret_cast<int*>(s_bits + uint32_t(C) * ALLOC);
+  if (blockIdx.x == 0 && blockIdx.y == 0) {
+    clear_shared_words(out_pyr, n_trees, L);
+    for (int64_t i = threadIdx.x; i < zero_words; i += BUILD_BLOCK) zero_cube[i] = 0u;
+  }
+  const int r = blockIdx.y;
+  const int y0 = int((int64_t(r) * H + R - 1) / R), y1 = int((int64_t(r + 1) * H + R - 1) / R);
+  const int W16 = W / 16;
+  const int64_t band_units = int64_t(y1 - y0) * W16;
+  const int64_t total = band_units * n_frames_used;
+  const int64_t b_begin = int64_t(blockIdx.x) * per_cta;
+  const int64_t b_end = min(total, b_begin + per_cta);
+  if (b_begin >= b_end) return;
+  if (threadIdx.x <= C) s_cb[threadIdx.x] = int((int64_t(threadIdx.x) * W + C - 1) / C);
+  for (uint32_t c = 0; c < uint32_t(C); ++c)
+    for (uint32_t i = threadIdx.x; i < Smem<L>::compact; i += BUILD_BLOCK) s_bits[c * ALLOC + Smem<L>::compact_word(i)] = 0u;
+  __syncthreads();
+  const int64_t upf = int64_t(H) * W16;
+  const int64_t upt = band_units * group_size;                  // band units per tree
+  const int lane = threadIdx.x & 31;
+  const int32_t rel0 = int32_t(threadIdx.x) - lane;
+  int64_t b = b_begin;
+  while (b < b_end) {
+    const int64_t grp = b / upt;
+    const int64_t seg_end = min(b_end, (grp + 1) * upt);
+    while (b < seg_end) {                                       // contiguous pieces: one frame each
+      const int64_t f = b / band_units, k0 = b - f * band_units;
+      const int64_t piece_end = min(seg_end, (f + 1) * band_units);
+      const int64_t len = piece_end - b;
+      const int64_t ubase = f * upf + int64_t(y0) * W16 + k0;
+      const int32_t n_it = len > rel0 ? int32_t((len - rel0 + BUILD_BLOCK - 1) / BUILD_BLOCK) : 0;
+      for (int32_t it = 0; it < n_it; ++it) {
+        const int64_t rel = int64_t(it) * BUILD_BLOCK + rel0 + lane;
+        const bool valid = rel < len;
+        uint32_t w[12];
+        if (valid) load_unit(frames, ubase + rel, w);
+        else {
+#pragma unroll
+          for (int q = 0; q < 12; ++q) w[q] = 0u;
+        }
+        const int x0 = int((k0 + rel) % W16) * 16;
+        int c = 0;
+        while (c + 1 < C && x0 >= s_cb[c + 1]) ++c;
+        const bool cut = x0 + 15 >= s_cb[c + 1];
+        build_unit_band<L>(w, valid && !cut, uint32_t(c) * (ALLOC * 4u));
+        if (valid && cut) build_unit_band_px<L>(w, x0, s_cb, C);
+      }
+      b = piece_end;
+    }
+    const bool last = seg_end >= b_end;
+    for (int c = 0; c < C; ++c)
+      flush_segment<L, BUILD_BLOCK>(s_bits + c * ALLOC, ws + (grp * R * C + int64_t(r) * C + c) * WSW, levels_out,
+                                    last);
+    if (last) break;
+    __syncthreads();
+  }
+}
+
+template <int L>
+static int launch_build_band(const uint8_t* frames, int n_frames_used, int H, int W, int R, int C, int group_size,
+                             uint32_t* ws, uint32_t* out_pyr, int64_t n_trees, uint32_t* zero_cube, int64_t zero_words,
+                             cudaStream_t st, int levels_out) {
+  const size_t smem = size_t(C) * BandBits<L>::ALLOC * 4 + 17 * 4;
+  static int attr_smem = 0;
+  if (int(smem) > attr_smem) {
+    CUDA_TRY(cudaFuncSetAttribute(k_build_band<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr_smem = int(smem);
+  }
+  const int64_t band_units = (int64_t(H) / R + 1) * (W / 16);
+  const int64_t per_band = (int64_t(sm_count()) + R - 1) / R;   // one CTA per SM in total
+  int64_t per_cta = (band_units * n_frames_used + per_band - 1) / per_band;
+  const int64_t min_per_cta = int64_t(BUILD_BLOCK) * 4;
+  if (per_cta < min_per_cta) per_cta = min_per_cta;
+  const int64_t gx = (band_units * n_frames_used + per_cta - 1) / per_cta;
+  k_build_band<L><<<dim3(unsigned(gx), unsigned(R)), BUILD_BLOCK, smem, st>>>(
+      frames, n_frames_used, H, W, R, C, group_size, per_cta, ws, out_pyr, n_trees, zero_cube, zero_words, levels_out);
+  LAUNCH_CHECK("k_build_band");
+  return OBG_OK;
+}
+
+// ---------------------------------------------------------------------------
 // K1 for L = 5 (and 4) with a BYTE per leaf (32 / 4 KB table): a pixel's leaf
 // is recorded with one plain byte store of 1 -- idempotent, so no lookup,
 // no warp vote, no miss path and no atomics (the bit-per-leaf K1 spends
@@ -2102,6 +2245,114 @@ k_classify_l7(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_pix
   flush_conf<OUT>(acc, counts);
 }
 
+// Region grid (R x C > 1, model.py:61-75), L <= 6, W % 16 == 0: blockIdx.y =
+// region row r (a band of rows, region_bounds); the CTA holds the C operands
+// of the band in shared memory (row layout, OPW words apart) and streams the
+// band's 16-pixel units.  A unit lies in one column region unless a column
+// boundary cuts it (at most C-1 units per row): those take a per-pixel path.
+constexpr int BAND_BLOCK = 512;
+template <int L>
+struct BandOp {
+  static constexpr uint32_t OPW = (uint32_t(SmemC<L>::words) + 31u) & ~31u;   // words per region operand
+};
+
+template <int L, int OUT>
+__global__ void __launch_bounds__(BAND_BLOCK)
+k_classify_band(const uint8_t* __restrict__ frames, int n_frames, int H, int W, int R, int C,
+                const uint32_t* __restrict__ cube, uint8_t* __restrict__ mask, unsigned long long* counts) {
+  using LY = SmemC<L>;
+  constexpr uint32_t OPW = BandOp<L>::OPW;
+  extern __shared__ uint32_t s_ops[];
+  __shared__ int s_cb[17];
+  ConfAcc acc;
+  const int r = blockIdx.y;
+  const int y0 = int((int64_t(r) * H + R - 1) / R), y1 = int((int64_t(r + 1) * H + R - 1) / R);
+  if (threadIdx.x <= C) s_cb[threadIdx.x] = int((int64_t(threadIdx.x) * W + C - 1) / C);
+  for (uint32_t c = 0; c < uint32_t(C); ++c) {
+    const uint32_t* src = cube + (int64_t(r) * C + c) * operand_words(L);
+    for (uint32_t i = threadIdx.x; i < LY::compact; i += BAND_BLOCK) {
+      const uint32_t p = LY::compact_word(i);
+      s_ops[c * OPW + p] = smem_word_from_cube<LY>(src, p);
+    }
+  }
+  __syncthreads();
+  const int W16 = W / 16;
+  const int64_t upf = int64_t(H) * W16;                         // units per frame
+  const int band_units = (y1 - y0) * W16;
+  const char* sb = reinterpret_cast<const char*>(s_ops);
+  for (int f = 0; f < n_frames; ++f) {
+    const int64_t ubase = int64_t(f) * upf + int64_t(y0) * W16;
+    const int stride = int(gridDim.x) * BAND_BLOCK;
+    for (int k0 = int(blockIdx.x) * BAND_BLOCK + int(threadIdx.x); k0 < band_units; k0 += 2 * stride) {
+      // two units per iteration: six 16-byte loads in flight
+      uint32_t wa[12], wb[12];
+      const bool second = k0 + stride < band_units;
+      load_unit(frames, ubase + k0, wa);
+      if (second) load_unit(frames, ubase + k0 + stride, wb);
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+      if (h == 1 && !second) break;
+      const int k = h ? k0 + stride : k0;
+      const int64_t u = ubase + k;
+      const int x0 = (k % W16) * 16;
+      int c = 0;
+      while (c + 1 < C && x0 >= s_cb[c + 1]) ++c;
+      uint32_t w[12];
+#pragma unroll
+      for (int q = 0; q < 12; ++q) w[q] = h ? wb[q] : wa[q];
+      uint32_t v[16];
+      if (x0 + 15 < s_cb[c + 1]) {
+        const char* base = sb + c * (OPW * 4u);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          uint32_t aa, ba, ab, bb;
+          pair_positions_dyn<LY>(w, kk, 0u, aa, ba, ab, bb);
+          const uint32_t wa = *reinterpret_cast<const uint32_t*>(base + aa);
+          const uint32_t wb = *reinterpret_cast<const uint32_t*>(base + ab);
+          v[2 * kk] = __funnelshift_r(wa, wa, ba);
+          v[2 * kk + 1] = __funnelshift_r(wb, wb, bb);
+        }
+      } else {
+        // a column boundary cuts the unit: region per pixel
+        uint32_t px[16];
+        unpack16<0, L>(w, px);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          int cj = 0;
+          while (cj + 1 < C && x0 + j >= s_cb[cj + 1]) ++cj;
+          uint32_t addr, bsel;
+          bit_position<L, LY>(px[j], addr, bsel);
+          const uint32_t wd = *reinterpret_cast<const uint32_t*>(sb + cj * (OPW * 4u) + addr);
+          v[j] = __funnelshift_r(wd, wd, bsel);
+        }
+      }
+      emit16<OUT>(v, mask, u, acc);
+      }
+    }
+  }
+  flush_conf<OUT>(acc, counts);
+}
+
+template <int L, int OUT>
+static int launch_classify_band(const uint8_t* frames, int n_frames, int H, int W, int R, int C, const uint32_t* cube,
+                                uint8_t* mask, unsigned long long* counts, cudaStream_t st) {
+  const size_t smem = size_t(C) * BandOp<L>::OPW * 4;
+  static int attr_smem = 0;
+  if (int(smem) > attr_smem) {
+    CUDA_TRY(cudaFuncSetAttribute(k_classify_band<L, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr_smem = int(smem);
+  }
+  const int bps = occupancy(k_classify_band<L, OUT>, BAND_BLOCK, smem);
+  const int64_t per_band = (int64_t(sm_count()) * bps + R - 1) / R;
+  const int64_t band_units = (int64_t(H) / R + 1) * (W / 16);
+  int64_t gx = min(per_band, (band_units + BAND_BLOCK - 1) / BAND_BLOCK);
+  if (gx < 1) gx = 1;
+  k_classify_band<L, OUT><<<dim3(unsigned(gx), unsigned(R)), BAND_BLOCK, smem, st>>>(frames, n_frames, H, W, R, C, cube,
+                                                                                    mask, counts);
+  LAUNCH_CHECK("k_classify_band");
+  return OBG_OK;
+}
+
 // Generic path: any grid / alignment / frame size.  One thread = 8 pixels of
 // one frame (one packed byte, or 8 u8 mask bytes).
 template <int OUT>
@@ -2534,7 +2785,10 @@ static int build_presence_impl(const uint8_t* frames, int n_frames, int height, 
   // trees whose leading pyramid words K1 clears for k_pyramid's atomics
   const int64_t clear_trees = cube_levels ? 0 : n_trees;
   // flat L <= 6: K1 writes the cube-order upper levels itself (k_build_flat flush)
-  const int smem_levels = (cube_levels && flat && levels <= 6) ? 1 : 0;
+  const bool band = !flat && n_regions > 1 && levels <= 6 && !out_counts && (width % 16) == 0 &&
+                    (reinterpret_cast<uintptr_t>(frames) % 16) == 0 && grid_cols <= 16 &&
+                    int64_t(grid_cols) * 4 * (levels == 6 ? BandBits<6>::ALLOC : BandBits<5>::ALLOC) + 68 <= 227 * 1024;
+  const int smem_levels = (cube_levels && (flat || band) && levels <= 6) ? 1 : 0;
   // The workspace is handed back all-zero by k_pyramid; a caller that keeps
   // it (OBG_WS_ZEROED) skips the clear.  Output pyramids need no memset: every
   // word is either stored once or (leading shared words) cleared by K1.
@@ -2557,6 +2811,16 @@ static int build_presence_impl(const uint8_t* frames, int n_frames, int height, 
                                            zero_cube, zero_words, st);
         break;
       default: rc = launch_build_flat<8>(frames, upf, total_units, group_size, ws, out_pyramids, clear_trees, zero_cube, zero_words, out_counts, st, smem_levels); break;
+    }
+  } else if (band) {
+    const int nf = n_groups * group_size;
+    switch (levels) {
+      case 1: rc = launch_build_band<1>(frames, nf, height, width, grid_rows, grid_cols, group_size, ws, out_pyramids, clear_trees, zero_cube, zero_words, st, smem_levels); break;
+      case 2: rc = launch_build_band<2>(frames, nf, height, width, grid_rows, grid_cols, group_size, ws, out_pyramids, clear_trees, zero_cube, zero_words, st, smem_levels); break;
+      case 3: rc = launch_build_band<3>(frames, nf, height, width, grid_rows, grid_cols, group_size, ws, out_pyramids, clear_trees, zero_cube, zero_words, st, smem_levels); break;
+      case 4: rc = launch_build_band<4>(frames, nf, height, width, grid_rows, grid_cols, group_size, ws, out_pyramids, clear_trees, zero_cube, zero_words, st, smem_levels); break;
+      case 5: rc = launch_build_band<5>(frames, nf, height, width, grid_rows, grid_cols, group_size, ws, out_pyramids, clear_trees, zero_cube, zero_words, st, smem_levels); break;
+      default: rc = launch_build_band<6>(frames, nf, height, width, grid_rows, grid_cols, group_size, ws, out_pyramids, clear_trees, zero_cube, zero_words, st, smem_levels); break;
     }
   } else {
     const int grid = grid_for(used_pixels, 256, sm_count() * 8);
@@ -2769,6 +3033,19 @@ static int classify_dispatch(const uint8_t* frames, int n_frames, int height, in
       case 6: return launch_classify_flat<6, OUT>(frames, n_pixels, cube_bits, mask, counts, st);
       case 7: return launch_classify_l7<OUT>(frames, n_pixels, cube_bits, mask, counts, st);
       default: return launch_classify_flat<8, OUT>(frames, n_pixels, cube_bits, mask, counts, st);
+    }
+  }
+  const bool band = (grid_rows > 1 || grid_cols > 1) && levels <= 6 && (width % 16) == 0 && aligned &&
+                    grid_cols <= 16 && grid_rows <= height &&
+                    size_t(grid_cols) * 4 * (levels == 6 ? BandOp<6>::OPW : BandOp<5>::OPW) <= 227 * 1024;
+  if (band) {
+    switch (levels) {
+      case 1: return launch_classify_band<1, OUT>(frames, n_frames, height, width, grid_rows, grid_cols, cube_bits, mask, counts, st);
+      case 2: return launch_classify_band<2, OUT>(frames, n_frames, height, width, grid_rows, grid_cols, cube_bits, mask, counts, st);
+      case 3: return launch_classify_band<3, OUT>(frames, n_frames, height, width, grid_rows, grid_cols, cube_bits, mask, counts, st);
+      case 4: return launch_classify_band<4, OUT>(frames, n_frames, height, width, grid_rows, grid_cols, cube_bits, mask, counts, st);
+      case 5: return launch_classify_band<5, OUT>(frames, n_frames, height, width, grid_rows, grid_cols, cube_bits, mask, counts, st);
+      default: return launch_classify_band<6, OUT>(frames, n_frames, height, width, grid_rows, grid_cols, cube_bits, mask, counts, st);
     }
   }
   const int64_t threads = ((P + 7) / 8) * n_frames;

@@ -434,3 +434,53 @@ def test_build_model_many_trees(cuda):
         model = obg.build_background_model_device(cuda.from_numpy(frames).cuda(), cfg)
         want = orc.build_background_model(list(frames), levels, thr)
         assert model.trees[0][0].to_bytes() == orc.to_bytes(want[(0, 0)])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("grid", [(2, 3), (3, 5), (4, 1), (1, 6), (5, 7)])
+@pytest.mark.parametrize("levels", [3, 5, 6])
+def test_region_grid_band_classify(cuda, grid, levels):
+    """Region grids with W % 16 == 0 take the band kernels (one bitset /
+    operand per column region in shared memory, units cut by a column
+    boundary per pixel): merged trees (groups of 1 and 2), a per-region frame
+    tree, masks (u8 and bit-packed) and fused confusion counts against the
+    oracle."""
+    rng = np.random.default_rng(levels * 100 + grid[0] * 10 + grid[1])
+    h, w = 50, 96
+    base = rng.integers(0, 256, size=(1, h, w, 3))
+    train = np.clip(base + rng.integers(-20, 21, size=(9, h, w, 3)), 0, 255).astype(np.uint8)
+    probe = np.clip(base + rng.integers(-40, 41, size=(5, h, w, 3)), 0, 255).astype(np.uint8)
+    probe[:, 5:30, 10:70] = rng.integers(0, 256, size=3).astype(np.uint8)
+    R, C = grid
+    cfg = ModelConfig(levels=levels, threshold=0.5, grid_rows=R, grid_cols=C, training_frames=9)
+    model = obg.build_background_model(list(train), cfg)
+    want_model = orc.build_background_model(list(train), levels, 0.5, R, C)
+    for r in range(R):                       # band build kernel: every region's merged tree
+        for c in range(C):
+            assert model.trees[r][c].to_bytes() == orc.to_bytes(want_model[(r, c)]), (r, c)
+    # groups of 2 frames + per-frame trees (obg_build_presence through the band kernel)
+    cfg2 = ModelConfig(levels=levels, threshold=0.5, grid_rows=R, grid_cols=C, group_size=2, training_frames=9)
+    m2 = obg.build_background_model(list(train), cfg2)
+    w2 = orc.build_background_model(list(train), levels, 0.5, R, C, group_size=2)
+    for r in range(R):
+        for c in range(C):
+            assert m2.trees[r][c].to_bytes() == orc.to_bytes(w2[(r, c)]), ("group 2", r, c)
+    pyr = obg.build_presence(cuda.from_numpy(train[:3]).cuda(), levels, R, C, 1)
+    for g in range(3):
+        for r, c in ((0, 0), (R - 1, C // 2), (R // 2, C - 1)):
+            want = orc.build_frame_tree([train[g]], (r, c), levels, R, C)
+            assert Octree._from_device(pyr[g, r * C + c], levels).to_bytes() == orc.to_bytes(want), (g, r, c)
+    dev = cuda.from_numpy(probe).cuda()
+    masks = obg.classify(model, dev).cpu().numpy()
+    packed = obg.classify(model, dev, packed=True).cpu().numpy()
+    truth = (rng.random((5, h, w)) < 0.4).astype(np.uint8)
+    counts = obg.classify_confusion(model, dev, cuda.from_numpy(truth).cuda())
+    tn = tp = fn = fp = 0
+    for i in range(len(probe)):
+        want = orc.detect_octree(want_model, probe[i], levels, R, C)
+        assert np.array_equal(masks[i].astype(bool), want), i
+        assert np.array_equal(np.unpackbits(packed[i], bitorder="little")[: h * w].astype(bool), want.ravel()), i
+        t = truth[i].astype(bool)
+        tp += int((want & t).sum()); fp += int((want & ~t).sum())
+        fn += int((~want & t).sum()); tn += int((~want & ~t).sum())
+    assert (counts.true_neg, counts.true_pos, counts.false_neg, counts.false_pos) == (tn, tp, fn, fp)
