@@ -2250,7 +2250,10 @@ k_classify_l7(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_pix
 // of the band in shared memory (row layout, OPW words apart) and streams the
 // band's 16-pixel units.  A unit lies in one column region unless a column
 // boundary cuts it (at most C-1 units per row): those take a per-pixel path.
-constexpr int BAND_BLOCK = 512;
+#ifndef OBG_BAND_BLOCK
+#define OBG_BAND_BLOCK 1024       // one CTA per SM holds the C operands; 1024 threads: 3x4 grid 177 -> 125 us
+#endif
+constexpr int BAND_BLOCK = OBG_BAND_BLOCK;
 template <int L>
 struct BandOp {
   static constexpr uint32_t OPW = (uint32_t(SmemC<L>::words) + 31u) & ~31u;   // words per region operand
