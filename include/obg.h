@@ -189,6 +189,20 @@ int obg_read_pnm_files(const char* const* paths, int n_files, int kind, int64_t 
 int obg_write_pgm_masks(const uint8_t* masks, int n_masks, int64_t width, int64_t height,
                         const char* const* paths, int n_threads);
 
+/* ---- sharded model build (distributed.py) -----------------
+ * Per-node tree counts of this rank's frames: the build of obg_build_model
+ * without its threshold.  counts: device u32 [R*C][pyramid_words][32], word w
+ * in the cube-order level layout (level_offset(l) + cube word), bit b at
+ * [w][b] -- sum them over ranks (all-reduce), then obg_threshold_counts with
+ * k_min from the global tree total gives every rank the merged model
+ * (out_merged path-order pyramids [R*C][PW], out_cube classify operands
+ * [R*C][obg_cube_words]). */
+int obg_build_counts(const uint8_t* frames, int n_frames, int height, int width, int levels,
+                     int grid_rows, int grid_cols, int group_size, uint32_t* counts,
+                     void* workspace, int64_t workspace_bytes, int flags, void* stream);
+int obg_threshold_counts(const uint32_t* counts, int n_regions, int levels, int64_t k_min,
+                         uint32_t* out_merged, uint32_t* out_cube, void* stream);
+
 /* ---- comparison baselines (detect.py:56-83) -------------------------------
  * Frame difference (detect_frame_diff, detect.py:56-63): mask i (u8 0/1,
  * [n_pairs][pixels]) is 1 where some channel of cur[i] differs from prev[i]

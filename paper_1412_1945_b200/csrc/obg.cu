@@ -24,7 +24,7 @@
 
 #include "../../include/obg.h"
 
-#define OBG_ABI_VERSION 4
+#define OBG_ABI_VERSION 5
 #define OBG_CUBE_ZEROED 0x100   /* internal: out_cube already cleared by the build kernel */
 
 // ---------------------------------------------------------------------------
@@ -1684,10 +1684,31 @@ constexpr int MERGE_GROUPS_C = OBG_MERGE_GROUPS;
 // Count word `off` (relative to tree 0 of the region; off < 0: no word) over
 // the trees of this thread's group and return the merged bits of the CTA's
 // 32-word slot x (valid in thread y == 0).  Zeroes what it reads.
+// MODE 0: merge (count + threshold); MODE 1: count only, the 32 per-bit
+// counts of the slot's word written to counts_w[0..31] (a sharded build's
+// partial counts, all-reduced across ranks); MODE 2: threshold counts_w
+// (no tree loads).
+template <int MODE>
 __device__ __forceinline__ uint32_t merge_slot(uint32_t* __restrict__ ws, int64_t off, int64_t stride, int n_groups,
                                                int64_t k_min, uint32_t (&s_acc)[MERGE_GROUPS_C][8][32],
-                                               uint32_t (&s_wide)[32][33], uint32_t (&s_bits)[8][32], bool wide) {
+                                               uint32_t (&s_wide)[32][33], uint32_t (&s_bits)[8][32], bool wide,
+                                               uint32_t* __restrict__ counts_w) {
   const int x = threadIdx.x, y = threadIdx.y;
+  if constexpr (MODE == 2) {
+    // counts of word x: bits from 32 u32 counts (one thread per word)
+    uint32_t bits = 0;
+    if (y == 0 && off >= 0) {
+      const uint4* src = reinterpret_cast<const uint4*>(counts_w);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint4 v = __ldcg(src + q);
+        bits |= (uint32_t(int64_t(v.x) >= k_min) << (4 * q)) | (uint32_t(int64_t(v.y) >= k_min) << (4 * q + 1)) |
+                (uint32_t(int64_t(v.z) >= k_min) << (4 * q + 2)) | (uint32_t(int64_t(v.w) >= k_min) << (4 * q + 3));
+      }
+    }
+    __syncthreads();
+    return bits;
+  }
   if (wide) {
     for (int i = y * 32 + x; i < 32 * 33; i += 32 * MERGE_GROUPS_C) (&s_wide[0][0])[i] = 0;
     __syncthreads();
@@ -1745,14 +1766,21 @@ __device__ __forceinline__ uint32_t merge_slot(uint32_t* __restrict__ ws, int64_
 #pragma unroll
       for (int j = 0; j < 4; ++j) c[j] += s_wide[x][y + 8 * j];
     }
-    uint32_t part = 0;
+    if constexpr (MODE == 1) {
+      if (off >= 0) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) part |= uint32_t(int64_t(c[j]) >= k_min) << (y + 8 * j);
-    s_bits[y][x] = part;
+        for (int j = 0; j < 4; ++j) counts_w[y + 8 * j] = c[j];
+      }
+    } else {
+      uint32_t part = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) part |= uint32_t(int64_t(c[j]) >= k_min) << (y + 8 * j);
+      s_bits[y][x] = part;
+    }
   }
   __syncthreads();
   uint32_t bits = 0;
-  if (y == 0) {
+  if (MODE == 0 && y == 0) {
 #pragma unroll
     for (int g = 0; g < 8; ++g) bits |= s_bits[g][x];
   }
@@ -1780,9 +1808,12 @@ __device__ __forceinline__ uint32_t mf_tile_word(int l, uint32_t t, uint32_t jj)
   return ((((R << l) + 4u * gq) << l) >> 5) + q;                    // rows (R, 4gq..4gq+3) are contiguous
 }
 
+// counts (MODE 1 out / MODE 2 in): u32 [n_regions][PW][32], word w of the
+// cube-order level layout (level_offset(l) + cube word), bit b at [w][b].
+template <int MODE>
 __global__ void __launch_bounds__(32 * MERGE_GROUPS_C)
 k_merge_fused(uint32_t* __restrict__ ws, int n_groups, int n_regions, int L, int64_t k_min,
-              uint32_t* __restrict__ cube, uint32_t* __restrict__ out) {
+              uint32_t* __restrict__ cube, uint32_t* __restrict__ out, uint32_t* __restrict__ counts) {
   __shared__ uint32_t s_acc[MERGE_GROUPS_C][8][32];
   __shared__ uint32_t s_wide[32][33];
   __shared__ uint32_t s_bits[8][32];
@@ -1803,7 +1834,9 @@ k_merge_fused(uint32_t* __restrict__ ws, int n_groups, int n_regions, int L, int
     int64_t off = -1;
     const int l = w == 0 ? 1 : 2;
     if (w < nw) off = (l == L) ? int64_t(w - level_offset(l)) : CW + w;
-    uint32_t bits = merge_slot(ws_r, off, stride, n_groups, k_min, s_acc, s_wide, s_bits, wide);
+    uint32_t bits = merge_slot<MODE>(ws_r, off, stride, n_groups, k_min, s_acc, s_wide, s_bits, wide,
+                                     counts + (r * PW + w) * 32);
+    if constexpr (MODE == 1) return;
     if (y == 0 && w < nw) {
       if (l == 1) bits &= 0xFFu;
       s_m[w] = bits;
@@ -1848,12 +1881,14 @@ k_merge_fused(uint32_t* __restrict__ ws, int n_groups, int n_regions, int L, int
       cw = mf_tile_word(l, g / WT, g % WT);
       off = (l == L) ? int64_t(cw) : CW + loff + cw;
     }
-    const uint32_t bits = merge_slot(ws_r, off, stride, n_groups, k_min, s_acc, s_wide, s_bits, wide);
-    if (y == 0 && g < LW) {
+    const uint32_t bits = merge_slot<MODE>(ws_r, off, stride, n_groups, k_min, s_acc, s_wide, s_bits, wide,
+                                           counts + (r * PW + loff + cw) * 32);
+    if (MODE != 1 && y == 0 && g < LW) {
       s_m[j] = bits;
       if (l == L) cube_r[cw] = bits;
     }
   }
+  if constexpr (MODE == 1) return;
   __syncthreads();
   if (uint32_t(tid) < NWc && slot0 + uint32_t(tid) < LW) {
     // path word: R>>1 = rp, G>>2 = gq, B>>2 = p; bit b0 + 2g0 + 4r0 + 8b1 + 16g1
@@ -2875,8 +2910,8 @@ int obg_build_model(const uint8_t* frames, int n_frames, int height, int width, 
   if (n_regions > 65535) return set_err(OBG_EUNSUPPORTED, "too many regions (%lld > 65535)", (long long)n_regions);
   int64_t blocks = 1;                                   // block 0: levels 1..2
   for (int l = 3; l <= levels; ++l) blocks += mf_blocks(l);
-  k_merge_fused<<<dim3(unsigned(blocks), unsigned(n_regions)), dim3(32, MERGE_GROUPS_C), 0, st>>>(
-      static_cast<uint32_t*>(workspace), n_groups, int(n_regions), levels, k_min, out_cube, out_merged);
+  k_merge_fused<0><<<dim3(unsigned(blocks), unsigned(n_regions)), dim3(32, MERGE_GROUPS_C), 0, st>>>(
+      static_cast<uint32_t*>(workspace), n_groups, int(n_regions), levels, k_min, out_cube, out_merged, nullptr);
   LAUNCH_CHECK("k_merge_fused");
   (void)words;
   return finish_operand(out_cube, n_regions, levels, st);
@@ -3190,4 +3225,50 @@ int obg_running_average(const uint8_t* frames, int n_frames, int64_t pixels, int
       frames, n_frames, pixels, frames_seen, average, double(diff_threshold), masks);
   LAUNCH_CHECK("k_running_average");
   return OBG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Sharded model build (distributed.py): the cube-order
+// build + per-node tree counts of this rank's frames; after an all-reduce of
+// the counts, the threshold + path-order conversion.
+// ---------------------------------------------------------------------------
+static int64_t merge_blocks(int levels) {
+  int64_t blocks = 1;
+  for (int l = 3; l <= levels; ++l) blocks += mf_blocks(l);
+  return blocks;
+}
+
+int obg_build_counts(const uint8_t* frames, int n_frames, int height, int width, int levels, int grid_rows,
+                     int grid_cols, int group_size, uint32_t* counts, void* workspace, int64_t workspace_bytes,
+                     int flags, void* stream) {
+  g_err[0] = 0;
+  if (levels < 1 || levels > 8) return set_err(OBG_EINVAL, "levels must be in 1..8, got %d", levels);
+  if (!counts) return set_err(OBG_EINVAL, "null buffer");
+  const int64_t n_regions = int64_t(grid_rows) * grid_cols;
+  if (n_regions > 65535) return set_err(OBG_EUNSUPPORTED, "too many regions (%lld > 65535)", (long long)n_regions);
+  // tree_pyramids: K1's leading-word clears need a target; the counts buffer
+  // is fully overwritten afterwards, so it doubles as that scratch
+  int rc = build_presence_impl(frames, n_frames, height, width, levels, grid_rows, grid_cols, group_size, counts,
+                               nullptr, workspace, workspace_bytes, flags, nullptr, 0, stream, /*cube_levels=*/true);
+  if (rc != OBG_OK) return rc;
+  cudaStream_t st = as_stream(stream);
+  const int n_groups = n_frames / group_size;
+  k_merge_fused<1><<<dim3(unsigned(merge_blocks(levels)), unsigned(n_regions)), dim3(32, MERGE_GROUPS_C), 0, st>>>(
+      static_cast<uint32_t*>(workspace), n_groups, int(n_regions), levels, 0, nullptr, nullptr, counts);
+  LAUNCH_CHECK("k_merge_fused<count>");
+  return OBG_OK;
+}
+
+int obg_threshold_counts(const uint32_t* counts, int n_regions, int levels, int64_t k_min, uint32_t* out_merged,
+                         uint32_t* out_cube, void* stream) {
+  g_err[0] = 0;
+  if (levels < 1 || levels > 8) return set_err(OBG_EINVAL, "levels must be in 1..8, got %d", levels);
+  if (n_regions < 1 || n_regions > 65535) return set_err(OBG_EINVAL, "n_regions must be in 1..65535");
+  if (k_min < 1) return set_err(OBG_EINVAL, "k_min must be >= 1, got %lld", (long long)k_min);
+  if (!counts || !out_merged || !out_cube) return set_err(OBG_EINVAL, "null buffer");
+  cudaStream_t st = as_stream(stream);
+  k_merge_fused<2><<<dim3(unsigned(merge_blocks(levels)), unsigned(n_regions)), dim3(32, MERGE_GROUPS_C), 0, st>>>(
+      nullptr, 0, n_regions, levels, k_min, out_cube, out_merged, const_cast<uint32_t*>(counts));
+  LAUNCH_CHECK("k_merge_fused<threshold>");
+  return finish_operand(out_cube, n_regions, levels, st);
 }

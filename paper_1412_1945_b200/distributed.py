@@ -1,12 +1,12 @@
 """Multi-GPU training of one background model.
 
 Training frames are independent units: each rank builds the per-(group,
-region) trees of its own shard with obg_build_presence and counts, per node,
-how many of its trees hold it (obg_merge_counts).  The only exchange is one
+region) trees of its own shard and counts, per node, how many of its trees
+hold it (obg_build_counts).  The only exchange is one
 all-reduce(SUM) of those counts plus the tree total; every rank then applies
 the reference's threshold locally (obg_merge_threshold), so all ranks end up
 with the identical merged model -- the one the reference would build from the
-concatenation of the shards (merge_trees is permutation invariant,
+concatenation of the shards (obg_threshold_counts) (merge_trees is permutation invariant,
 reference tests/test_model.py:154-161).
 
 Classification needs no communication: each rank classifies its own frames
@@ -16,7 +16,7 @@ against its replica of the (small) merged model.
 from __future__ import annotations
 
 from . import _device, _lib
-from .model import BackgroundModel, ModelConfig, build_presence, merge_k_min
+from .model import BackgroundModel, ModelConfig, merge_k_min
 
 
 def allreduce_counts(counts, n_trees: int, group=None):
@@ -40,20 +40,33 @@ def build_background_model_sharded(frames_dev, config: ModelConfig, group=None, 
     Every rank's shard must hold whole groups (its length is floored to a
     multiple of ``group_size``).  ``global_trees`` (the total number of trees
     over all ranks) may be passed to skip the scalar all-reduce; ``k_min`` is
-    computed from it exactly as the reference's float test (model.py:152)."""
+    computed from it exactly as the reference's float test (model.py:152).
+
+    Device path: ``obg_build_counts`` (the cube-order build of
+    ``obg_build_model`` with per-node tree counts instead of its threshold),
+    one all-reduce(SUM) of the counts, ``obg_threshold_counts`` (threshold +
+    path-order conversion + classify operand)."""
+    from .model import _WORKSPACES, _workspace
     n, h, w = int(frames_dev.shape[0]), int(frames_dev.shape[1]), int(frames_dev.shape[2])
     n_groups = n // config.group_size
     if n_groups == 0:
         raise ValueError(f"need at least {config.group_size} frames for one group, got {n}")
     L = config.levels
-    n_regions = config.grid_rows * config.grid_cols
-    pyr = build_presence(frames_dev[: n_groups * config.group_size], L, config.grid_rows, config.grid_cols,
-                         config.group_size)
-    pw = _lib.pyramid_words(L)
-    counts = _device.empty((n_regions, pw * 32), "int32")
+    R, C, gs = config.grid_rows, config.grid_cols, config.group_size
+    n_regions = R * C
     lib = _lib.load()
-    _lib.check(lib.obg_merge_counts(_device.ptr(pyr), n_groups, n_regions, L, _device.ptr(counts),
-                                    _device.stream_handle()))
+    pw = _lib.pyramid_words(L)
+    frames_dev = _device.to_device_u8(frames_dev[: n_groups * gs])
+    counts = _device.empty((n_regions, pw * 32), "int32")
+    ws_bytes = lib.obg_build_workspace_bytes(n_groups, n_regions, L)
+    stream = _device.stream_handle()
+    ws = _workspace(ws_bytes, stream)
+    try:
+        _lib.check(lib.obg_build_counts(_device.ptr(frames_dev), n_groups * gs, h, w, L, R, C, gs,
+                                        _device.ptr(counts), _device.ptr(ws), ws_bytes, _lib.WS_ZEROED, stream))
+    except Exception:
+        _WORKSPACES.pop((_device.torch().cuda.current_device(), stream), None)
+        raise
     if global_trees is None:
         total = allreduce_counts(counts, n_groups, group)
     else:
@@ -64,7 +77,6 @@ def build_background_model_sharded(frames_dev, config: ModelConfig, group=None, 
     k_min = merge_k_min(total, config.threshold)
     merged = _device.empty((n_regions, pw), "int32")
     cube = _device.empty((n_regions, _lib.cube_words(L)), "int32")
-    _lib.check(lib.obg_merge_threshold(_device.ptr(counts), n_regions, L, k_min, _device.ptr(merged),
-                                       _device.ptr(cube), _device.stream_handle()))
+    _lib.check(lib.obg_threshold_counts(_device.ptr(counts), n_regions, L, k_min, _device.ptr(merged),
+                                        _device.ptr(cube), stream))
     return BackgroundModel(config, frame_width=w, frame_height=h, _device_pyramids=merged, _device_cube=cube)
-

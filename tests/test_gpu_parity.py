@@ -484,3 +484,48 @@ def test_region_grid_band_classify(cuda, grid, levels):
         tp += int((want & t).sum()); fp += int((want & ~t).sum())
         fn += int((~want & t).sum()); tn += int((~want & ~t).sum())
     assert (counts.true_neg, counts.true_pos, counts.false_neg, counts.false_pos) == (tn, tp, fn, fp)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("levels,grid,gs", [(4, (1, 1), 1), (5, (1, 1), 2), (6, (1, 1), 1), (6, (2, 3), 1), (3, (3, 2), 2)])
+def test_sharded_build_counts(cuda, levels, grid, gs):
+    """The multi-GPU build path on one GPU: obg_build_counts on two shards,
+    the counts summed as the NCCL all-reduce would, obg_threshold_counts with
+    the global k_min -> every region's merged tree equals the reference's merge
+    of all frames; build_background_model_sharded (no process group) likewise."""
+    from paper_1412_1945_b200 import _device
+    from paper_1412_1945_b200.distributed import build_background_model_sharded
+    rng = np.random.default_rng(levels * 31 + gs)
+    h, w = 40, 64
+    base = rng.integers(0, 256, size=(1, h, w, 3))
+    frames = np.clip(base + rng.integers(-30, 31, size=(12, h, w, 3)), 0, 255).astype(np.uint8)
+    R, C = grid
+    thr = 0.5
+    cfg = ModelConfig(levels=levels, threshold=thr, grid_rows=R, grid_cols=C, group_size=gs, training_frames=12)
+    want = orc.build_background_model(list(frames), levels, thr, R, C, group_size=gs)
+    lib = _lib.load()
+    pw = _lib.pyramid_words(levels)
+    total = cuda.zeros((R * C, pw * 32), dtype=cuda.int32, device="cuda")
+    for shard in (frames[:6], frames[6:]):
+        dev = cuda.from_numpy(np.ascontiguousarray(shard)).cuda()
+        counts = cuda.empty((R * C, pw * 32), dtype=cuda.int32, device="cuda")
+        ng = len(shard) // gs
+        wsb = lib.obg_build_workspace_bytes(ng, R * C, levels)
+        ws = cuda.zeros((wsb + 3) // 4, dtype=cuda.int32, device="cuda")
+        _lib.check(lib.obg_build_counts(_device.ptr(dev), ng * gs, h, w, levels, R, C, gs, _device.ptr(counts),
+                                        _device.ptr(ws), wsb, _lib.WS_ZEROED, _device.stream_handle()))
+        assert int(ws.abs().sum()) == 0            # workspace handed back zeroed
+        total += counts
+    k_min = obg.merge_k_min(12 // gs, thr)
+    merged = cuda.empty((R * C, pw), dtype=cuda.int32, device="cuda")
+    cube = cuda.empty((R * C, _lib.cube_words(levels)), dtype=cuda.int32, device="cuda")
+    _lib.check(lib.obg_threshold_counts(_device.ptr(total), R * C, levels, k_min, _device.ptr(merged),
+                                        _device.ptr(cube), _device.stream_handle()))
+    model = obg.BackgroundModel(cfg, frame_width=w, frame_height=h, _device_pyramids=merged, _device_cube=cube)
+    single = build_background_model_sharded(cuda.from_numpy(frames).cuda(), cfg)
+    for r in range(R):
+        for c in range(C):
+            assert model.trees[r][c].to_bytes() == orc.to_bytes(want[(r, c)]), (r, c)
+            assert single.trees[r][c].to_bytes() == orc.to_bytes(want[(r, c)]), (r, c)
+    probe = frames[3]
+    assert np.array_equal(obg.detect_octree(model, probe), orc.detect_octree(want, probe, levels, R, C))

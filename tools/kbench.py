@@ -56,7 +56,7 @@ def timeit(fn, reps=20):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["build", "classify", "model", "confusion", "framediff", "runavg"])
+    ap.add_argument("what", choices=["build", "classify", "model", "sharded", "confusion", "framediff", "runavg"])
     ap.add_argument("--frames", type=int, default=64)
     ap.add_argument("--scene", default="c3")
     ap.add_argument("--levels", type=int, default=6)
@@ -78,6 +78,9 @@ def main():
         model = obg.build_background_model_device(f, cfg)
         truth = (torch.rand(f.shape[:3], device="cuda") < 0.3).to(torch.uint8)
         ms = timeit(lambda: obg.classify_confusion(model, f, truth))
+    elif a.what == "sharded":        # the multi-GPU build path (counts + threshold), no process group
+        from paper_1412_1945_b200.distributed import build_background_model_sharded
+        ms = timeit(lambda: build_background_model_sharded(f, cfg))
     elif a.what == "framediff":      # consecutive-pair masks, every frame read once (4 B/px)
         out = torch.empty((f.shape[0] - 1,) + tuple(f.shape[1:3]), dtype=torch.uint8, device="cuda")
         ms = timeit(lambda: obg.frame_diff_sequence(f, 30, out=out))
