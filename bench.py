@@ -427,7 +427,8 @@ def run_ours(args):
     L = cfg.levels
     flat = (P % 16) == 0 and cfg.grid_rows * cfg.grid_cols == 1
     # obg_build_model's kernels (include/obg.h) + obg_classify's
-    launches = {("k_build_generic" if not flat else "k_build_l7h" if L == 7 else "k_build_flat"): 1}
+    launches = {("k_build_generic" if not flat else "k_build_l7h" if L == 7 else "k_build_bytes" if L == 5
+                 else "k_build_flat"): 1}
     if L >= 7 or not flat:
         launches["k_levels_cube"] = 1
     launches["k_merge_fused"] = 1
@@ -437,9 +438,9 @@ def run_ours(args):
     if not flat:
         cls_kernel = "k_classify_generic"
     launches[cls_kernel] = 1
-    if world > 1:   # sharded build (distributed.py): presence + counts, all-reduce, threshold
-        launches = {("k_build_flat" if flat else "k_build_generic"): 1, "k_pyramid": 1, "k_merge(counts)": 1,
-                    "k_threshold": 1, cls_kernel: 1}
+    if world > 1:   # sharded build (distributed.py): counts, all-reduce (NCCL), threshold
+        build_k = {k: v for k, v in launches.items() if k not in ("k_merge_fused", cls_kernel, "k_l7_states")}
+        launches = dict(build_k, **{"k_merge_fused<count>": 1, "k_merge_fused<threshold>": 1, cls_kernel: 1})
         if L == 7:
             launches["k_l7_states"] = 1
     cls_bytes = n_test * P * 4                 # 3 B read + 1 B mask written per pixel
