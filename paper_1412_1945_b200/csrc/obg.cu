@@ -1985,7 +1985,10 @@ __global__ void k_l7_states(uint32_t* __restrict__ operand, int64_t n_regions) {
 // ===========================================================================
 // K4  classify
 // ===========================================================================
-constexpr int CLS_BLOCK = 256;
+#ifndef OBG_CLS_BLOCK
+#define OBG_CLS_BLOCK 256
+#endif
+constexpr int CLS_BLOCK = OBG_CLS_BLOCK;
 
 // Flat path: 1x1 grid, leaf cube bitset in shared memory (L <= 6) or read
 // through L1/L2 (L >= 7).  One thread = one 16-pixel unit per iteration:
