@@ -189,6 +189,15 @@ int obg_read_pnm_files(const char* const* paths, int n_files, int kind, int64_t 
 int obg_write_pgm_masks(const uint8_t* masks, int n_masks, int64_t width, int64_t height,
                         const char* const* paths, int n_threads);
 
+/* Parse one non-empty preorder child-mask tree (Octree.from_bytes /
+ * decode_tree, octree.py:229-237, 250-281) at data[pos..n) into a host
+ * path-order pyramid (u32 [obg_pyramid_words(depth)]).  On OBG_EFORMAT,
+ * *err_kind is 0 ("truncated octree data") or 1 ("octree node below leaf
+ * depth") and *err_offset the reference's byte offset; *end_pos is the byte
+ * after the tree.  Host only. */
+int obg_decode_tree(const uint8_t* data, int64_t n, int64_t pos, int depth, uint32_t* pyramid,
+                    int64_t* end_pos, int64_t* err_offset, int* err_kind);
+
 /* ---- sharded model build (distributed.py) -----------------
  * Per-node tree counts of this rank's frames: the build of obg_build_model
  * without its threshold.  counts: device u32 [R*C][pyramid_words][32], word w

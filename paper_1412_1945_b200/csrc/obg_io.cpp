@@ -301,3 +301,45 @@ int obg_write_pgm_masks(const uint8_t* masks, int n_masks, int64_t width, int64_
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Octree.from_bytes / decode_tree (reference octree.py:229-237, 250-281):
+// iterative preorder walk over child-mask bytes, the reference's error order
+// and offsets, node bits straight into the path-order pyramid.
+// ---------------------------------------------------------------------------
+static int64_t io_level_words(int l) { return l <= 1 ? 1 : (int64_t(1) << (3 * l - 5)); }
+static int64_t io_level_offset(int l) {
+  int64_t off = 0;
+  for (int m = 1; m < l; ++m) off += io_level_words(m);
+  return off;
+}
+
+int obg_decode_tree(const uint8_t* data, int64_t n, int64_t pos, int depth, uint32_t* pyramid, int64_t* end_pos,
+                    int64_t* err_offset, int* err_kind) {
+  if (depth < 1 || depth > 8 || !data || !pyramid || !end_pos || !err_offset || !err_kind) return OBG_EINVAL;
+  *err_kind = 0;
+  int64_t off[9];
+  for (int l = 1; l <= depth; ++l) off[l] = io_level_offset(l);
+  const int64_t pw = io_level_offset(depth + 1);
+  memset(pyramid, 0, size_t(pw) * 4);
+  if (pos >= n) { *err_offset = pos; *err_kind = 0; return OBG_EFORMAT; }
+  struct Frame { int level; uint32_t prefix; uint32_t rem; };
+  Frame stack[10];
+  int sp = 0;
+  stack[sp++] = Frame{0, 0u, data[pos++]};
+  while (sp > 0) {
+    Frame& top = stack[sp - 1];
+    if (top.rem == 0) { --sp; continue; }
+    const uint32_t low = top.rem & (0u - top.rem);
+    top.rem ^= low;
+    const int child_level = top.level + 1;
+    const uint32_t child = top.prefix * 8u + uint32_t(__builtin_ctz(low));
+    if (pos >= n) { *err_offset = pos; *err_kind = 0; return OBG_EFORMAT; }      // truncated octree data
+    const uint32_t m = data[pos++];
+    if (child_level == depth && m != 0) { *err_offset = pos - 1; *err_kind = 1; return OBG_EFORMAT; }
+    pyramid[off[child_level] + (child >> 5)] |= 1u << (child & 31u);
+    if (child_level < depth) stack[sp++] = Frame{child_level, child, m};
+  }
+  *end_pos = pos;
+  return OBG_OK;
+}

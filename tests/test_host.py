@@ -237,3 +237,38 @@ def test_golden_model_files_parse(golden, case):
     """Reference-written OBGM files parse and re-serialise byte-identically."""
     blob = bytes.fromhex(golden["random_cases"][case]["model_file"])
     assert obg.write_model(obg.read_model(blob)) == blob
+
+
+def test_native_decode_tree_matches_python_walk():
+    """obg_decode_tree (native) vs the Python preorder walk on valid trees,
+    truncations and corrupted bytes: same pyramid and end position, or the
+    same FormatError message and offset."""
+    from paper_1412_1945_b200 import _lib
+    from paper_1412_1945_b200.errors import FormatError
+    from paper_1412_1945_b200.octree import _decode_tree_native, _decode_tree_py
+    try:
+        _lib.load()
+    except Exception:
+        pytest.skip("libobg.so not built")
+    rng = np.random.default_rng(99)
+    for case in range(300):
+        depth = int(rng.integers(1, 6))
+        codes = rng.integers(0, 8 ** depth, size=int(rng.integers(1, 40)))
+        from oracle import octree_oracle as orc
+        blob = bytearray(orc.to_bytes(orc.tree_from_codes(codes, depth)))
+        kind = case % 4
+        if kind == 1:
+            blob = blob[: int(rng.integers(0, len(blob)))]
+        elif kind == 2 and len(blob) > 1:
+            blob[int(rng.integers(0, len(blob)))] = int(rng.integers(0, 256))
+        elif kind == 3:
+            blob += bytes(rng.integers(0, 256, size=3).astype(np.uint8))
+        data = bytes(blob)
+        results = []
+        for fn in (_decode_tree_native, _decode_tree_py):
+            try:
+                tree, end = fn(data, 0, depth)
+                results.append(("ok", tree._host().tobytes(), end))
+            except FormatError as e:
+                results.append(("err", str(e), e.offset))
+        assert results[0] == results[1], (case, results)
