@@ -378,6 +378,17 @@ static int sm_count() {
   return g_sm_count[dev];
 }
 
+// Per-device cache of one-time launch setup (the dynamic-smem opt-in and
+// occupancy are per device): cache() is the slot of the current device.
+struct DevCache {
+  int v[64] = {0};
+  int& operator()() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= 64) d = 0;
+    return v[d];
+  }
+};
+
 template <typename K>
 static int occupancy(K kernel, int block, size_t smem) {
   int n = 0;
@@ -998,10 +1009,10 @@ static int launch_build_band(const uint8_t* frames, int n_frames_used, int H, in
                              uint32_t* ws, uint32_t* out_pyr, int64_t n_trees, uint32_t* zero_cube, int64_t zero_words,
                              cudaStream_t st, int levels_out) {
   const size_t smem = size_t(C) * BandBits<L>::ALLOC * 4 + 17 * 4;
-  static int attr_smem = 0;
-  if (int(smem) > attr_smem) {
+  static DevCache attr_smem;
+  if (int(smem) > attr_smem()) {
     CUDA_TRY(cudaFuncSetAttribute(k_build_band<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr_smem = int(smem);
+    attr_smem() = int(smem);
   }
   const int64_t band_units = (int64_t(H) / R + 1) * (W / 16);
   const int64_t per_band = (int64_t(sm_count()) + R - 1) / R;   // one CTA per SM in total
@@ -2378,10 +2389,10 @@ template <int L, int OUT>
 static int launch_classify_band(const uint8_t* frames, int n_frames, int H, int W, int R, int C, const uint32_t* cube,
                                 uint8_t* mask, unsigned long long* counts, cudaStream_t st) {
   const size_t smem = size_t(C) * BandOp<L>::OPW * 4;
-  static int attr_smem = 0;
-  if (int(smem) > attr_smem) {
+  static DevCache attr_smem;
+  if (int(smem) > attr_smem()) {
     CUDA_TRY(cudaFuncSetAttribute(k_classify_band<L, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr_smem = int(smem);
+    attr_smem() = int(smem);
   }
   const int bps = occupancy(k_classify_band<L, OUT>, BAND_BLOCK, smem);
   const int64_t per_band = (int64_t(sm_count()) * bps + R - 1) / R;
@@ -2707,8 +2718,8 @@ static int launch_build_flat(const uint8_t* frames, int64_t units_per_frame, int
   constexpr bool SMEM = L <= 6;
   const size_t smem = SMEM ? size_t(Smem<L>::alloc_words) * 4 : 0;
   // one-time per instantiation: opt in to > 48 KB dynamic smem, cache occupancy
-  static int occ[2] = {0, 0};
-  int& blocks_per_sm = occ[counts ? 1 : 0];
+  static DevCache occ[2];
+  int& blocks_per_sm = occ[counts ? 1 : 0]();
   if (blocks_per_sm == 0) {
     if (counts) {
       auto k = k_build_flat<L, SMEM, true>;
@@ -2735,10 +2746,10 @@ static int launch_build_flat(const uint8_t* frames, int64_t units_per_frame, int
   if constexpr (L == 5) {
     if (!counts) {
       const size_t smem_b = ByteTab<L>::BITS_OFF + size_t(Smem<L>::alloc_words) * 4;
-      static bool attr = false;
-      if (!attr) {
+      static DevCache attr;
+      if (!attr()) {
         CUDA_TRY(cudaFuncSetAttribute(k_build_bytes<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_b)));
-        attr = true;
+        attr() = 1;
       }
       k_build_bytes<L><<<grid, BUILD_BLOCK, smem_b, st>>>(frames, units_per_frame, total_units, group_size, per_cta,
                                                           ws, out_pyr, n_trees, zero_cube, zero_words, levels_out);
@@ -2761,10 +2772,10 @@ static int launch_build_l7h(const uint8_t* frames, int64_t units_per_frame, int6
                             uint32_t* ws, uint32_t* out_pyr, int64_t n_trees, uint32_t* zero_cube, int64_t zero_words,
                             cudaStream_t st) {
   constexpr size_t smem = size_t(L7H_ALLOC) * 4;
-  static bool attr = false;
-  if (!attr) {
+  static DevCache attr;
+  if (!attr()) {
     CUDA_TRY(cudaFuncSetAttribute(k_build_l7h, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr = true;
+    attr() = 1;
   }
   const int64_t max_ctas = sm_count();                   // one CTA per SM
   int64_t per_cta = (total_units + max_ctas - 1) / max_ctas;
@@ -3018,7 +3029,8 @@ static int launch_classify_flat(const uint8_t* frames, int64_t n_pixels, const u
   constexpr bool SMEM = L <= 6;
   const size_t smem = SMEM ? size_t(SmemC<L>::words) * 4 : 0;
   const int64_t n_units = n_pixels / 16;
-  static int bps = 0;                        // per instantiation: opt in to > 48 KB smem, occupancy
+  static DevCache bps_cache;                 // per instantiation and device: smem opt-in, occupancy
+  int& bps = bps_cache();
   if (bps == 0) {
     CUDA_TRY(cudaFuncSetAttribute(k_classify_flat<L, SMEM, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(smem)));
@@ -3037,7 +3049,8 @@ template <int OUT>
 static int launch_classify_l7(const uint8_t* frames, int64_t n_pixels, const uint32_t* cube, uint8_t* mask,
                               unsigned long long* counts, cudaStream_t st) {
   const size_t smem = size_t(S7_WORDS) * 4;
-  static int bps = 0;
+  static DevCache bps_cache;
+  int& bps = bps_cache();
   if (bps == 0) {
     CUDA_TRY(cudaFuncSetAttribute(k_classify_l7<OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     bps = occupancy(k_classify_l7<OUT>, S7_BLOCK, smem);
