@@ -1190,37 +1190,64 @@ constexpr uint32_t L7H_ROWW = 512 + 5;                 // words per R' row (128 
 constexpr uint32_t L7H_WORDS = 64 * L7H_ROWW;          // one half of the cube
 constexpr uint32_t L7H_ALLOC = L7H_WORDS + 32;         // + per-lane dummy words
 
-// x = [*, G, B, R]: byte offset in the half-cube, bit selector, half of R'
-__device__ __forceinline__ void l7h_position(uint32_t x, uint32_t& off, uint32_t& bsel, uint32_t& half) {
-  const uint32_t r6 = __umulhi(x, 1u << 7) & 63u;                          // (x >> 25) & 63
-  const uint32_t g = __umulhi(x, 1u << 27) & 0x7F0u;                       // G' << 4
-  const uint32_t b = __umulhi(x, 1u << 12) & 0xCu;                         // (B' >> 5) << 2
-  off = r6 * (L7H_ROWW * 4u) + (g | b);
-  bsel = __umulhi(x, 1u << 15);                                           // x >> 17: B' in the low bits
-  half = x >> 31;
-}
 
 // Returns nonzero if some pixel of the unit lies in the other half (so the
 // CTA needs its second pass).
 #ifndef OBG_L7_TRACK
 #define OBG_L7_TRACK 2
 #endif
+// Half-cube word offsets of pixels 2K and 2K+1, two at a time (as
+// pair_positions): word offsets R6 * ROWW + G' * 4 + B' >> 5 are < 64 K, so
+// both ride in the 16-bit halves of one register; byte addresses come out of
+// the split.  mis_* bit 0 = the pixel lies in the other half (a "hit").
+template <int K>
+__device__ __forceinline__ void l7h_pair(const uint32_t (&w)[12], uint32_t hmask, uint32_t& addr_a, uint32_t& bsel_a,
+                                         uint32_t& mis_a, uint32_t& addr_b, uint32_t& bsel_b, uint32_t& mis_b) {
+  constexpr int o = 6 * K, a = o >> 2, b = o & 3;
+  constexpr uint32_t selR = uint32_t(b) | (uint32_t(b) << 4) | (uint32_t(b + 3) << 8) | (uint32_t(b + 3) << 12);
+  constexpr uint32_t selG = uint32_t(b + 1) | (uint32_t(b + 2) << 4) | (uint32_t(b + 4) << 8) | (uint32_t(b + 5) << 12);
+  const uint32_t yR = __byte_perm(w[a], w[a + 1], selR);                 // [R_A, R_A, R_B, R_B]
+  const uint32_t yG = __byte_perm(w[a], w[a + 1], selG);                 // [G_A, B_A, G_B, B_B]
+  const uint32_t P = __umulhi(yR, 1u << 31) & 0x003F003Fu;               // (R >> 1) & 63 per half
+  const uint32_t bq = __umulhi(yG, 1u << 18) & 0x00030003u;              // B >> 6 per half
+  const uint32_t q = (yG & 0x00FE00FEu) * 2u + bq;                       // G' * 4 + B' >> 5
+  const uint32_t pair = P * L7H_ROWW + q;                                // word offsets
+  addr_b = __umulhi(pair, 1u << 18) & ~3u;                               // (pair >> 16) * 4
+  addr_a = (pair << 2) & 0x3FFFCu;                                       // (pair & 0xFFFF) * 4
+  bsel_a = __umulhi(yG, 1u << 23);                                       // yG >> 9: B_A' low bits
+  bsel_b = __umulhi(yG, 1u << 7);                                        // yG >> 25
+  const uint32_t hx = yR ^ hmask;                                        // R top bit vs the pass's half
+  mis_a = hx >> 7;
+  mis_b = hx >> 23;
+}
+
+template <int K>
+__device__ __forceinline__ void l7h_pair_dyn(const uint32_t (&w)[12], int k, uint32_t hmask, uint32_t& aa,
+                                             uint32_t& ba, uint32_t& ma, uint32_t& ab, uint32_t& bb, uint32_t& mb) {
+  switch (k) {
+    case 0: l7h_pair<0>(w, hmask, aa, ba, ma, ab, bb, mb); break;
+    case 1: l7h_pair<1>(w, hmask, aa, ba, ma, ab, bb, mb); break;
+    case 2: l7h_pair<2>(w, hmask, aa, ba, ma, ab, bb, mb); break;
+    case 3: l7h_pair<3>(w, hmask, aa, ba, ma, ab, bb, mb); break;
+    case 4: l7h_pair<4>(w, hmask, aa, ba, ma, ab, bb, mb); break;
+    case 5: l7h_pair<5>(w, hmask, aa, ba, ma, ab, bb, mb); break;
+    case 6: l7h_pair<6>(w, hmask, aa, ba, ma, ab, bb, mb); break;
+    default: l7h_pair<7>(w, hmask, aa, ba, ma, ab, bb, mb); break;
+  }
+}
+
 __device__ __forceinline__ uint32_t build_unit_l7h(const uint32_t (&w)[12], uint32_t hpass, bool valid) {
-  uint32_t px[16];
-  unpack16<0, 6>(w, px);                                                  // [*, G, B, R] operands
   uint32_t other = 0;
+  const uint32_t hmask = hpass ? 0xFFFFFFFFu : 0u;
 #pragma unroll
   for (int g = 0; g < 16; g += 4) {
-    uint32_t addr[4], bsel[4], v[4];
+    uint32_t addr[4], bsel[4], v[4], mis[4];
+    l7h_pair_dyn<0>(w, g / 2, hmask, addr[0], bsel[0], mis[0], addr[1], bsel[1], mis[1]);
+    l7h_pair_dyn<0>(w, g / 2 + 1, hmask, addr[2], bsel[2], mis[2], addr[3], bsel[3], mis[3]);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      uint32_t half;
-      l7h_position(px[g + j], addr[j], bsel[j], half);
       const uint32_t wd = lds_at(addr[j]);
-#if OBG_L7_TRACK == 1
-      other |= half ^ hpass;
-#endif
-      v[j] = __funnelshift_r(wd, wd, bsel[j]) | (half ^ hpass);            // other half: a hit
+      v[j] = __funnelshift_r(wd, wd, bsel[j]) | mis[j];                  // other half: a hit
     }
     const bool miss = valid && !(v[0] & v[1] & v[2] & v[3] & 1u);
     if (__any_sync(0xFFFFFFFFu, miss)) {
