@@ -1193,9 +1193,6 @@ constexpr uint32_t L7H_ALLOC = L7H_WORDS + 32;         // + per-lane dummy words
 
 // Returns nonzero if some pixel of the unit lies in the other half (so the
 // CTA needs its second pass).
-#ifndef OBG_L7_TRACK
-#define OBG_L7_TRACK 2
-#endif
 // Half-cube word offsets of pixels 2K and 2K+1, two at a time (as
 // pair_positions): word offsets R6 * ROWW + G' * 4 + B' >> 5 are < 64 K, so
 // both ride in the 16-bit halves of one register; byte addresses come out of
@@ -1255,7 +1252,6 @@ __device__ __forceinline__ uint32_t build_unit_l7h(const uint32_t (&w)[12], uint
       for (int j = 0; j < 4; ++j) reds_or_if(addr[j], 1u << (bsel[j] & 31u), valid ? (v[j] & 1u) : 1u);
     }
   }
-#if OBG_L7_TRACK == 2
   // R bytes of the 16 pixels sit at bytes 0, 3, 6, 9 of each 12-byte group:
   // top bits 0x80000080 / 0x00800000 / 0x00008000 of words 3q, 3q+1, 3q+2
   const uint32_t x0 = hpass ? 0xFFFFFFFFu : 0u;
@@ -1263,7 +1259,6 @@ __device__ __forceinline__ uint32_t build_unit_l7h(const uint32_t (&w)[12], uint
   const uint32_t o1 = (w[1] ^ x0) | (w[4] ^ x0) | (w[7] ^ x0) | (w[10] ^ x0);
   const uint32_t o2 = (w[2] ^ x0) | (w[5] ^ x0) | (w[8] ^ x0) | (w[11] ^ x0);
   other = (o0 & 0x80000080u) | (o1 & 0x00800000u) | (o2 & 0x00008000u);
-#endif
   return valid ? other : 0u;
 }
 
@@ -1291,9 +1286,6 @@ k_build_l7h(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t
   const uint32_t h_first = uint32_t(__ldg(frames + 48 * u_begin)) >> 7;
   uint32_t need_other = 0;
   for (uint32_t pass = 0; pass < 2; ++pass) {
-#if OBG_L7_TRACK == 0
-    need_other = 1;
-#endif
     if (pass == 1 && !__syncthreads_or(int(need_other))) break;
     const uint32_t h = pass == 0 ? h_first : 1u - h_first;
     int64_t u = u_begin;
