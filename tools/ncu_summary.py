@@ -52,4 +52,7 @@ def main(path):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    try:
+        main(sys.argv[1])
+    except BrokenPipeError:      # piped into head
+        pass
