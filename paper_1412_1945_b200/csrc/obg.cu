@@ -2327,6 +2327,45 @@ struct BandOp {
   static constexpr uint32_t OPW = (uint32_t(SmemC<L>::words) + 31u) & ~31u;   // words per region operand
 };
 
+// one unit of a band: column region (or per-pixel regions where a boundary
+// cuts it), lookups in that region's shared operand, 16 mask bytes / bits
+template <int L, int OUT>
+__device__ __forceinline__ void band_unit(const uint32_t (&w)[12], int k, int64_t ubase, int W16, int C,
+                                          const int* s_cb, const char* sb, uint8_t* mask, ConfAcc& acc) {
+  using LY = SmemC<L>;
+  constexpr uint32_t OPW = BandOp<L>::OPW;
+  const int x0 = (k % W16) * 16;
+  int c = 0;
+  while (c + 1 < C && x0 >= s_cb[c + 1]) ++c;
+  uint32_t v[16];
+  if (x0 + 15 < s_cb[c + 1]) {
+    const char* base = sb + c * (OPW * 4u);
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      uint32_t aa, ba, ab, bb;
+      pair_positions_dyn<LY>(w, kk, 0u, aa, ba, ab, bb);
+      const uint32_t xa = *reinterpret_cast<const uint32_t*>(base + aa);
+      const uint32_t xb = *reinterpret_cast<const uint32_t*>(base + ab);
+      v[2 * kk] = __funnelshift_r(xa, xa, ba);
+      v[2 * kk + 1] = __funnelshift_r(xb, xb, bb);
+    }
+  } else {
+    // a column boundary cuts the unit: region per pixel
+    uint32_t px[16];
+    unpack16<0, L>(w, px);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      int cj = 0;
+      while (cj + 1 < C && x0 + j >= s_cb[cj + 1]) ++cj;
+      uint32_t addr, bsel;
+      bit_position<L, LY>(px[j], addr, bsel);
+      const uint32_t wd = *reinterpret_cast<const uint32_t*>(sb + cj * (OPW * 4u) + addr);
+      v[j] = __funnelshift_r(wd, wd, bsel);
+    }
+  }
+  emit16<OUT>(v, mask, ubase + k, acc);
+}
+
 template <int L, int OUT>
 __global__ void __launch_bounds__(BAND_BLOCK)
 k_classify_band(const uint8_t* __restrict__ frames, int n_frames, int H, int W, int R, int C,
@@ -2360,45 +2399,8 @@ k_classify_band(const uint8_t* __restrict__ frames, int n_frames, int H, int W, 
       const bool second = k0 + stride < band_units;
       load_unit(frames, ubase + k0, wa);
       if (second) load_unit(frames, ubase + k0 + stride, wb);
-#pragma unroll 1
-      for (int h = 0; h < 2; ++h) {
-      if (h == 1 && !second) break;
-      const int k = h ? k0 + stride : k0;
-      const int64_t u = ubase + k;
-      const int x0 = (k % W16) * 16;
-      int c = 0;
-      while (c + 1 < C && x0 >= s_cb[c + 1]) ++c;
-      uint32_t w[12];
-#pragma unroll
-      for (int q = 0; q < 12; ++q) w[q] = h ? wb[q] : wa[q];
-      uint32_t v[16];
-      if (x0 + 15 < s_cb[c + 1]) {
-        const char* base = sb + c * (OPW * 4u);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          uint32_t aa, ba, ab, bb;
-          pair_positions_dyn<LY>(w, kk, 0u, aa, ba, ab, bb);
-          const uint32_t wa = *reinterpret_cast<const uint32_t*>(base + aa);
-          const uint32_t wb = *reinterpret_cast<const uint32_t*>(base + ab);
-          v[2 * kk] = __funnelshift_r(wa, wa, ba);
-          v[2 * kk + 1] = __funnelshift_r(wb, wb, bb);
-        }
-      } else {
-        // a column boundary cuts the unit: region per pixel
-        uint32_t px[16];
-        unpack16<0, L>(w, px);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          int cj = 0;
-          while (cj + 1 < C && x0 + j >= s_cb[cj + 1]) ++cj;
-          uint32_t addr, bsel;
-          bit_position<L, LY>(px[j], addr, bsel);
-          const uint32_t wd = *reinterpret_cast<const uint32_t*>(sb + cj * (OPW * 4u) + addr);
-          v[j] = __funnelshift_r(wd, wd, bsel);
-        }
-      }
-      emit16<OUT>(v, mask, u, acc);
-      }
+      band_unit<L, OUT>(wa, k0, ubase, W16, C, s_cb, sb, mask, acc);
+      if (second) band_unit<L, OUT>(wb, k0 + stride, ubase, W16, C, s_cb, sb, mask, acc);
     }
   }
   flush_conf<OUT>(acc, counts);
