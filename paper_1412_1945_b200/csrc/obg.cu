@@ -1031,18 +1031,21 @@ static int launch_build_band(const uint8_t* frames, int n_frames_used, int H, in
 // is recorded with one plain byte store of 1 -- idempotent, so no lookup,
 // no warp vote, no miss path and no atomics (the bit-per-leaf K1 spends
 // ~8 instructions per pixel on lookup + test + vote, and its miss path on
-// every first sighting).  Row layout: byte R' * RS + G' * 2^L + B', rows of
-// RS = 4^L + 16 bytes (16-byte aligned; 4 pad words skew R' across banks).
+// every first sighting).  Row layout: byte R' * RS + G' * GS + B', RS =
+// 2^L * GS + 16 bytes (the 16-byte pad skews R' across banks; GS below).
 // At a tree boundary the table is packed into the bit-per-leaf row layout
 // (Smem<L>, right after the table) and flushed by flush_segment as before.
 // ---------------------------------------------------------------------------
 template <int L>
 struct ByteTab {
   static constexpr int s = 8 - L;
-  static constexpr uint32_t RS = (1u << (2 * L)) + 16u;          // bytes per R' row
+  // bytes per G' row: L = 5 pads the 32-byte rows to 40 (10 words: G' rows
+  // 16 apart share a bank instead of 4; the G' term becomes one IMAD by 5)
+  static constexpr uint32_t GS = L == 5 ? 40u : (1u << L);
+  static constexpr uint32_t RS = (1u << L) * GS + 16u;           // bytes per R' row
   static constexpr uint32_t BYTES = (1u << L) * RS;
   static constexpr uint32_t BITS_OFF = (BYTES + 1023u) & ~1023u;  // byte offset of the Smem<L> bitset
-  static_assert(RS % (1u << s) == 0 && RS % 16 == 0, "row stride");
+  static_assert(RS % (1u << s) == 0 && RS % 16 == 0 && GS % 8 == 0, "row strides");
 };
 
 // byte offsets of pixels 2K and 2K+1 of a unit in the table
@@ -1060,7 +1063,8 @@ __device__ __forceinline__ void byte_pair(const uint32_t (&w)[12], uint32_t& a, 
   const uint32_t gq = yG & ((M << s) | (M << (s + 16)));           // G & ~(2^s-1): G' << s
   const uint32_t bq = (yG >> (8 + s)) & (M | (M << 16));           // B'
   uint32_t q;
-  if constexpr (2 * L - 8 >= 0) q = (gq << (2 * L - 8)) | bq;      // G' << L | B'
+  if constexpr (L == 5) q = gq * 5u + bq;                         // G' * 40 + B' (gq = G' << 3)
+  else if constexpr (2 * L - 8 >= 0) q = (gq << (2 * L - 8)) | bq; // G' << L | B'
   else q = (gq >> (8 - 2 * L)) | bq;
   const uint32_t pair = P * (T::RS >> s) + q;
   b = __umulhi(pair, 1u << 16);
@@ -1105,13 +1109,13 @@ __device__ __forceinline__ void pack_byte_table(uint32_t* s_tab, uint32_t* s_bit
   constexpr uint32_t ROWS = 1u << (2 * L);                         // (R', G') rows of 2^L bytes
   for (uint32_t r = threadIdx.x; r < ROWS; r += BUILD_BLOCK) {
     const uint32_t R = r >> L, G = r & ((1u << L) - 1u);
-    uint4* src = reinterpret_cast<uint4*>(reinterpret_cast<char*>(s_tab) + R * T::RS + (G << L));
+    uint2* src = reinterpret_cast<uint2*>(reinterpret_cast<char*>(s_tab) + R * T::RS + G * T::GS);
     uint32_t bits = 0;
 #pragma unroll
-    for (int v = 0; v < (1 << L) / 16; ++v) {
-      const uint4 q = src[v];
-      bits |= (pack4(q.x) | (pack4(q.y) << 4) | (pack4(q.z) << 8) | (pack4(q.w) << 12)) << (16 * v);
-      if (clear) src[v] = make_uint4(0u, 0u, 0u, 0u);
+    for (int v = 0; v < (1 << L) / 8; ++v) {                      // 8-byte pieces (rows are 8-byte aligned)
+      const uint2 q = src[v];
+      bits |= (pack4(q.x) | (pack4(q.y) << 4)) << (8 * v);
+      if (clear) src[v] = make_uint2(0u, 0u);
     }
     if constexpr (L == 5) s_bits[R * S::ROWW + G] = bits;
     else s_bits[R * S::ROWW + G] = bits * S::REP;                  // L = 4: 16-bit row replicated
