@@ -2145,7 +2145,10 @@ __device__ __forceinline__ void classify_unit(const uint32_t (&w)[12], const uin
 // `mask`: the output mask (OUT_U8 / OUT_PACKED) or the truth mask read by
 // the fused evaluation (OUT_CONF_*, counts += tn, tp, fn, fp).
 template <int L, bool SMEM_BITS, int OUT>
-__global__ void __launch_bounds__(CLS_BLOCK, 2)
+#ifndef OBG_CLS_MINB
+#define OBG_CLS_MINB 2           // 4 CTAs per SM at L6; 5 or 6 (48 / 40 regs) lose L1 to shared memory: +3 % / +35 %
+#endif
+__global__ void __launch_bounds__(CLS_BLOCK, OBG_CLS_MINB)
 k_classify_flat(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_pixels,
                 const uint32_t* __restrict__ cube, uint8_t* __restrict__ mask, unsigned long long* counts) {
   ConfAcc acc;
