@@ -157,16 +157,23 @@ def _pool_build(i):
     return ref.build_frame_tree([train[i]], (0, 0), cfg).to_bytes()
 
 
-def _pool_detect(i):
-    ref, test, model = _POOL_STATE["ref"], _POOL_STATE["test"], _POOL_STATE["model"]
-    return np.packbits(ref.detect_octree(model, test[i]))
+def _pool_detect(task):
+    """Detect a chunk of test frames with the merged tree sent as bytes (the
+    worker decodes it once per task; the pool is never re-forked)."""
+    blob, width, height, lo, hi = task
+    ref, test, cfg = _POOL_STATE["ref"], _POOL_STATE["test"], _POOL_STATE["cfg"]
+    tree = ref.Octree.from_bytes(blob, cfg.levels) if blob else ref.Octree(cfg.levels)
+    model = ref.BackgroundModel(cfg, width, height, [[tree]])
+    return [np.packbits(ref.detect_octree(model, test[i])) for i in range(lo, hi)]
 
 
 def cpu_reference_step(ref, train, test, cfg_kw, pool=None):
-    """One bounded sample of the workload through the reference's public API:
+    """One step of the workload through the reference's public API:
     build_background_model over ``train`` + detect_octree per ``test`` frame.
-    With a fork pool, per-frame trees / masks are computed in workers (trees
-    return via to_bytes), decode + merge stay serial (reference semantics)."""
+    With a (persistent) fork pool: per-frame trees are built in the workers
+    and return via to_bytes, decode + merge_trees stay serial (the reference's
+    merge is one call over all trees), and the merged tree goes back to the
+    workers as bytes for the per-frame detects (reference semantics)."""
     if ref is not None:
         cfg = ref.ModelConfig(**cfg_kw)
         if pool is None:
@@ -174,15 +181,15 @@ def cpu_reference_step(ref, train, test, cfg_kw, pool=None):
             for f in test:
                 ref.detect_octree(model, f)
             return
-        # `pool` was forked with ref/train/test/cfg in _POOL_STATE
         blobs = pool.map(_pool_build, range(len(train)))
         trees = [ref.Octree.from_bytes(b, cfg.levels) for b in blobs]
         merged = ref.merge_trees(trees, cfg.threshold, cfg.levels)
-        model = ref.BackgroundModel(cfg, train.shape[2], train.shape[1], [[merged]])
-        _POOL_STATE["model"] = model
-        from multiprocessing import get_context
-        with get_context("fork").Pool(pool._processes) as detect_pool:   # workers inherit the model
-            detect_pool.map(_pool_detect, range(len(test)))
+        blob = merged.to_bytes()
+        n, workers = len(test), pool._processes
+        bounds = [n * k // workers for k in range(workers + 1)]
+        tasks = [(blob, train.shape[2], train.shape[1], bounds[k], bounds[k + 1])
+                 for k in range(workers) if bounds[k + 1] > bounds[k]]
+        pool.map(_pool_detect, tasks)
         return
     from oracle import octree_oracle as orc   # port of the reference (no reference install present)
     model = orc.build_background_model(list(train), cfg_kw["levels"], cfg_kw["threshold"])
@@ -210,21 +217,34 @@ def cpu_baseline(scene, cfg_kw):
                       f"({statistics.median(times):.1f} s)"}
 
 
+def workload_config(scene, n_train, n_test, world=1):
+    """The ``config`` object both arms print (identical for the same workload)."""
+    P = scene.width * scene.height
+    return {"workload": workload_name(scene, n_train, n_test) + " (per rank)",
+            "frames_per_step": n_train + n_test, "pixels_per_step": (n_train + n_test) * P * world,
+            "parallelism": f"dp{world}",
+            "l2": f"inputs {(n_train + n_test) * P * 3 / 2**30:.2f} GiB per step > 126 MB L2 (no flush needed)"}
+
+
 def run_reference(args):
+    """The reference arm: the unmodified reference package (baseline/_ref)
+    through its public API on the SAME workload as our arm (same seeded 64
+    training + 256 test frames, same config), all host cores through one
+    persistent fork pool created before the timed steps."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from multiprocessing import get_context
     from paper_1412_1945_b200 import scenes
-    n_test = 64 if args.config != 4 else 4
-    scene = scenes.generate(args.config, seed=args.seed, n_test=n_test, levels=args.levels, variant=args.variant)
-    cfg_kw = dict(levels=scene.config.levels, threshold=scene.config.threshold,
-                  training_frames=len(scene.train))
+    scene = scenes.generate(args.config, seed=args.seed, levels=args.levels, variant=args.variant)
+    n_train, n_test = len(scene.train), len(scene.test)
+    cfg_kw = dict(levels=scene.config.levels, threshold=scene.config.threshold, training_frames=n_train)
     ref = _reference_module()
     cores = os.cpu_count() or 1
+    pool = None
     if ref is not None:
         _POOL_STATE.update(ref=ref, train=scene.train, test=scene.test, cfg=ref.ModelConfig(**cfg_kw))
-    pool = get_context("fork").Pool(cores) if ref is not None else None
+        pool = get_context("fork").Pool(cores)      # forked once: workers inherit the frames
     for _ in range(args.warmup):
         cpu_reference_step(ref, scene.train, scene.test, cfg_kw, pool)
     times = []
@@ -234,20 +254,24 @@ def run_reference(args):
         times.append(time.perf_counter() - t0)
     if pool is not None:
         pool.close()
-    px = (len(scene.train) + n_test) * scene.width * scene.height
+        pool.join()
+    px = (n_train + n_test) * scene.width * scene.height
     ms = 1000 * statistics.mean(times)
     value = px / (ms / 1000) / 1e6
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "Mpx/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic (seeded scenes with BASELINE config 3 shapes)",
-        "config": {"workload": workload_name(scene, len(scene.train), n_test) + " (bounded sample of the test batch)",
-                   "parallelism": f"fork pool x{cores}" if ref is not None else "1 process (oracle port)"},
+        "data": f"synthetic (seeded scene generator for BASELINE config {scene.config_id}: its frame shape, "
+                "depth, threshold and background/foreground distributions; paper_1412_1945_b200/scenes.py)",
+        "config": workload_config(scene, n_train, n_test),
+        "host": {"pool": f"persistent fork pool x{cores}" if ref is not None else "1 process (oracle port)",
+                 "method": "per-frame build_frame_tree in the workers (trees back via to_bytes), "
+                           "Octree.from_bytes + merge_trees serial, merged tree sent to the workers as bytes, "
+                           "detect_octree per frame in the workers"},
         "cpu_baseline": {"value": round(value, 3), "unit": "Mpx/s", "cores": cores if ref is not None else 1,
                          "kind": "reference" if ref is not None else "port",
-                         "sample": f"64 training + {n_test} test frames per step; per-frame trees and masks in "
-                                   "a fork pool over all host cores, decode + merge serial"},
+                         "sample": f"the whole workload: {n_train} training + {n_test} test frames per step"},
         "e2e": {"value": round(value, 3), "unit": "Mpx/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -335,7 +359,7 @@ def run_ours(args):
         # the timed steps: one graph replay each (build + classify, no gap)
         for _ in range(args.steps):
             captured.step()
-        model = captured.step_model
+        model = captured.model
     else:
         for k in range(args.steps):
             model = step(evs[k])
@@ -384,6 +408,7 @@ def run_ours(args):
         parity = {"merged_tree_vs_reference": ok_tree if world == 1 else None, "masks_vs_reference": ok_masks,
                   "frames": n_test}
 
+    peak, peak_src = peaks()
     # end to end through the public API: pinned host frames -> device -> host masks
     e2e = None
     if not args.no_e2e:
@@ -424,8 +449,47 @@ def run_ours(args):
                "path": "pipeline.process_batches: pinned host frames -> H2D (copy stream) -> build + classify "
                        "in 8-frame chunks -> mask D2H (second copy stream), copies overlapped with kernels"
                        if world == 1 else "eager H2D + sharded build + classify + D2H"}
+        # same-run PCIe ceiling: one pinned H2D copy of the step's frames
+        dst = torch.empty_like(h_test, device=dev)
+        for _ in range(2):
+            dst.copy_(h_test, non_blocking=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(3):
+            dst.copy_(h_test, non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        h2d_gbs = 3 * h_test.numel() / (a.elapsed_time(b) / 1000) / 1e9
+        del dst
+        e2e["h2d_ceiling_gbs"] = round(h2d_gbs, 2)
+        e2e["h2d_achieved_gbs"] = round(e2e["h2d_bytes_per_step"] / (e_ms / 1000) / 1e9, 2)
+        e2e["frac_of_h2d_ceiling"] = round(e2e["h2d_achieved_gbs"] / h2d_gbs, 3)
+        if world == 1:
+            # the literal reference signature (the way the reference's own
+            # bench times itself, cli.py:262-288): a list of numpy frames into
+            # build_background_model, then detect_octree per numpy frame --
+            # pageable host arrays, one synchronous call per frame
+            train_list, test_list = list(scene.train), list(scene.test)
 
-    peak, peak_src = peaks()
+            def sig_step():
+                model = obg.build_background_model(train_list, cfg)
+                for f in test_list:
+                    obg.detect_octree(model, f)
+
+            sig_step()
+            times = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                sig_step()
+                times.append(time.perf_counter() - t0)
+            sig_s = statistics.median(times)
+            e2e["reference_signature"] = {
+                "value": round(px_step / sig_s / 1e6, 3), "unit": "Mpx/s", "ms_per_step": round(1000 * sig_s, 2),
+                "h2d_bytes_per_step": int(h_train.numel() + h_test.numel()),
+                "d2h_bytes_per_step": int(h_masks.numel()),
+                "path": "build_background_model(list of 64 numpy frames) + detect_octree(model, frame) for each of "
+                        "256 numpy frames (reference API, host wall clock, median of 3)"}
+
     traffic = None
     try:   # dram read+write of the classify kernel from the committed ncu --set full capture
         with open(os.path.join(REPO, "profiles", "traffic.json")) as f:
@@ -458,6 +522,35 @@ def run_ours(args):
     cls_gbs = cls_bytes / (cls_avg / 1000) / 1e9
     build_gbs = build_bytes / (build_avg / 1000) / 1e9
 
+    # the build alone at the classify batch size (north_star: "classify and
+    # build each ... at 1920x1080x256-frame batches"): the 256 test frames as
+    # training frames, one captured build graph replayed K times back to back
+    build256 = None
+    if world == 1 and not args.eager:
+        from paper_1412_1945_b200.model import new_workspace
+        cfg256 = obg.ModelConfig(levels=cfg.levels, threshold=cfg.threshold, training_frames=n_test)
+        ws256 = new_workspace(obg._lib.load().obg_build_workspace_bytes(n_test, 1, cfg.levels))
+        for _ in range(2):
+            obg.build_background_model_device(test, cfg256, workspace=ws256)
+        torch.cuda.synchronize()
+        g256 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g256):
+            obg.build_background_model_device(test, cfg256, workspace=ws256)
+        g256.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            g256.replay()
+        b.record(stream)
+        torch.cuda.synchronize()
+        b256_ms = a.elapsed_time(b) / args.steps
+        b256_bytes = n_test * (P * 3 + obg._lib.cube_words(cfg.levels) * 4)
+        build256 = {"frames": n_test, "ms": round(b256_ms, 4),
+                    "mpx_s": round(n_test * P / (b256_ms / 1000) / 1e6, 1),
+                    "hbm_frac": round(b256_bytes / (b256_ms / 1000) / 1e9 / peak, 4)}
+        del g256, ws256
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(scene, dict(levels=cfg.levels, threshold=cfg.threshold, training_frames=n_train))
@@ -469,16 +562,16 @@ def run_ours(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": f"synthetic (seeded scene generator for BASELINE config {scene.config_id}: its frame shape, "
                     "depth, threshold and background/foreground distributions; paper_1412_1945_b200/scenes.py)",
-            "config": {"workload": workload_name(scene, n_train, n_test) + " (per rank)",
-                       "frames_per_step": n_train + n_test, "pixels_per_step": px_step * world,
-                       "parallelism": f"dp{world}" + (" (NCCL all-reduce of merge counts)" if world > 1 else ""),
-                       "launch": "one CUDA graph replay per step (build + classify); build_ms / classify_ms from K back-to-back replays of each half's graph" if captured else "eager",
-                       "l2": f"inputs {(n_train + n_test) * P * 3 / 2**30:.2f} GiB per step > 126 MB L2 "
-                             "(no flush needed)",
+            "config": workload_config(scene, n_train, n_test, world),
+            "phases": {"launch": "one CUDA graph replay per step (build + classify); build_ms / classify_ms from K "
+                                 "back-to-back replays of each half's graph" if captured else "eager",
+                       "all_reduce": "NCCL all-reduce of merge counts" if world > 1 else None,
                        "build_ms": round(build_avg, 4), "classify_ms": round(cls_avg, 4),
                        "build_mpx_s": round(n_train * P / (build_avg / 1000) / 1e6, 1),
                        "classify_mpx_s": round(n_test * P / (cls_avg / 1000) / 1e6, 1),
-                       "build_hbm_frac": round(build_gbs / peak, 4)},
+                       "build_hbm_frac": round(build_gbs / peak, 4),
+                       "build_hbm_bytes": build_bytes, "classify_hbm_bytes": cls_bytes,
+                       "build_256": build256},
             "roofline": {"bound": "hbm", "kernel": f"{cls_kernel} (obg_classify)",
                          "achieved": round(cls_gbs, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(cls_gbs / peak, 4), "traffic": traffic, "peak_source": peak_src,

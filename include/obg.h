@@ -198,6 +198,14 @@ int obg_write_pgm_masks(const uint8_t* masks, int n_masks, int64_t width, int64_
 int obg_decode_tree(const uint8_t* data, int64_t n, int64_t pos, int depth, uint32_t* pyramid,
                     int64_t* end_pos, int64_t* err_offset, int* err_kind);
 
+/* The same parse emitting the nodes below the root in preorder as
+ * codes[k] (path code) / levels[k] (1..depth), *n_nodes of them -- O(nodes)
+ * for sparse trees; each level's codes come out ascending.  capacity >=
+ * n - pos - 1 always suffices.  Errors as obg_decode_tree.  Host only. */
+int obg_decode_tree_codes(const uint8_t* data, int64_t n, int64_t pos, int depth, uint32_t* codes,
+                          uint8_t* levels, int64_t capacity, int64_t* n_nodes, int64_t* end_pos,
+                          int64_t* err_offset, int* err_kind);
+
 /* ---- sharded model build (distributed.py) -----------------
  * Per-node tree counts of this rank's frames: the build of obg_build_model
  * without its threshold.  counts: device u32 [R*C][pyramid_words][32], word w

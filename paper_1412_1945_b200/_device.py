@@ -54,6 +54,25 @@ def to_device_u8(frames):
     return t.from_numpy(arr).to("cuda")
 
 
+def frames_on_device(frames, what: str = "frames"):
+    """Validated (n, h, w, 3) uint8 frames as a contiguous CUDA tensor on the
+    current device, for the batched device entry points: a strided view is
+    made contiguous, host data (numpy / CPU tensor) is copied over, and a
+    tensor on another CUDA device is rejected -- the kernels take a raw
+    pointer and would otherwise read wrong pixels or fault."""
+    t = torch()
+    if isinstance(frames, t.Tensor):
+        shape, ok_dtype = tuple(frames.shape), frames.dtype == t.uint8
+        if frames.is_cuda and frames.device.index != t.cuda.current_device():
+            raise ValueError(f"{what} are on {frames.device}, the current device is cuda:{t.cuda.current_device()}")
+    else:
+        frames = np.asarray(frames)
+        shape, ok_dtype = frames.shape, frames.dtype == np.uint8
+    if len(shape) != 4 or shape[3] != 3 or not ok_dtype:
+        raise ValueError(f"{what}: expected (n, h, w, 3) uint8 frames, got {frames.dtype} {shape}")
+    return to_device_u8(frames)
+
+
 def to_device_u32(arr):
     t = torch()
     if isinstance(arr, t.Tensor):

@@ -58,12 +58,15 @@ SIGNATURES = {
     "obg_write_pgm_masks": (_I, [_P, _I, _L, _L, ctypes.POINTER(ctypes.c_char_p), _I]),
     "obg_decode_tree": (_I, [_P, _L, _L, _I, _P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
                              ctypes.POINTER(ctypes.c_int)]),
+    "obg_decode_tree_codes": (_I, [_P, _L, _L, _I, _P, _P, _L, ctypes.POINTER(ctypes.c_int64),
+                                   ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
+                                   ctypes.POINTER(ctypes.c_int)]),
     "obg_build_counts": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _L, _I, _P]),
     "obg_threshold_counts": (_I, [_P, _I, _I, _L, _P, _P, _P]),
     "obg_frame_diff": (_I, [_P, _P, _I, _L, _I, _P, _P]),
     "obg_running_average": (_I, [_P, _I, _L, _L, _P, _I, _P, _P]),
 }
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 
 class LibraryNotBuilt(RuntimeError):

@@ -24,7 +24,7 @@
 
 #include "../../include/obg.h"
 
-#define OBG_ABI_VERSION 6
+#define OBG_ABI_VERSION 7
 #define OBG_CUBE_ZEROED 0x100   /* internal: out_cube already cleared by the build kernel */
 
 // ---------------------------------------------------------------------------

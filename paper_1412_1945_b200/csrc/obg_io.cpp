@@ -343,3 +343,42 @@ int obg_decode_tree(const uint8_t* data, int64_t n, int64_t pos, int depth, uint
   *end_pos = pos;
   return OBG_OK;
 }
+
+// Same walk as obg_decode_tree, emitting the nodes below the root in preorder
+// as (code, level) pairs instead of a dense pyramid: O(nodes) for sparse
+// trees (a depth-8 pyramid is 2.4 MB however few nodes it holds).  Preorder
+// visits each level's nodes in ascending code order, so the codes of level l,
+// taken in output order, are already sorted.
+int obg_decode_tree_codes(const uint8_t* data, int64_t n, int64_t pos, int depth, uint32_t* codes,
+                          uint8_t* levels, int64_t capacity, int64_t* n_nodes, int64_t* end_pos,
+                          int64_t* err_offset, int* err_kind) {
+  if (depth < 1 || depth > 8 || !data || !n_nodes || !end_pos || !err_offset || !err_kind) return OBG_EINVAL;
+  if (capacity > 0 && (!codes || !levels)) return OBG_EINVAL;
+  *err_kind = 0;
+  *n_nodes = 0;
+  if (pos >= n) { *err_offset = pos; return OBG_EFORMAT; }
+  struct Frame { int level; uint32_t prefix; uint32_t rem; };
+  Frame stack[10];
+  int sp = 0;
+  int64_t k = 0;
+  stack[sp++] = Frame{0, 0u, data[pos++]};
+  while (sp > 0) {
+    Frame& top = stack[sp - 1];
+    if (top.rem == 0) { --sp; continue; }
+    const uint32_t low = top.rem & (0u - top.rem);
+    top.rem ^= low;
+    const int child_level = top.level + 1;
+    const uint32_t child = top.prefix * 8u + uint32_t(__builtin_ctz(low));
+    if (pos >= n) { *err_offset = pos; *err_kind = 0; return OBG_EFORMAT; }      // truncated octree data
+    const uint32_t m = data[pos++];
+    if (child_level == depth && m != 0) { *err_offset = pos - 1; *err_kind = 1; return OBG_EFORMAT; }
+    if (k >= capacity) return OBG_EINVAL;   // capacity < nodes: caller passes n - pos - 1
+    codes[k] = child;
+    levels[k] = uint8_t(child_level);
+    ++k;
+    if (child_level < depth) stack[sp++] = Frame{child_level, child, m};
+  }
+  *n_nodes = k;
+  *end_pos = pos;
+  return OBG_OK;
+}

@@ -27,6 +27,7 @@ def classify(model: BackgroundModel, frames_dev, out=None, packed: bool = False)
     A pixel is foreground iff its quantized colour is not a full-depth leaf
     of its region's merged tree; an empty tree flags everything (detect.py:44-52).
     """
+    frames_dev = _device.frames_on_device(frames_dev)
     n, h, w = int(frames_dev.shape[0]), int(frames_dev.shape[1]), int(frames_dev.shape[2])
     _check_frame_shape(model, h, w)
     cfg = model.config
@@ -66,7 +67,7 @@ def detect_octree(model: BackgroundModel, frame) -> np.ndarray:
 def detect_octree_batch(model: BackgroundModel, frames) -> np.ndarray:
     """``detect_octree`` over a (n, h, w, 3) batch in one launch -> (n, h, w) bool."""
     if _device.is_tensor(frames):
-        mask = classify(model, _device.to_device_u8(frames))
+        mask = classify(model, frames)
         return mask.view(_device.torch().bool)
     frames = np.asarray(frames)
     if frames.ndim != 4 or frames.shape[3] != 3 or frames.dtype != np.uint8:

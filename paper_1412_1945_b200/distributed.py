@@ -46,7 +46,8 @@ def build_background_model_sharded(frames_dev, config: ModelConfig, group=None, 
     ``obg_build_model`` with per-node tree counts instead of its threshold),
     one all-reduce(SUM) of the counts, ``obg_threshold_counts`` (threshold +
     path-order conversion + classify operand)."""
-    from .model import _WORKSPACES, _workspace
+    from .model import _drop_workspace, _workspace
+    frames_dev = _device.frames_on_device(frames_dev)
     n, h, w = int(frames_dev.shape[0]), int(frames_dev.shape[1]), int(frames_dev.shape[2])
     n_groups = n // config.group_size
     if n_groups == 0:
@@ -65,7 +66,7 @@ def build_background_model_sharded(frames_dev, config: ModelConfig, group=None, 
         _lib.check(lib.obg_build_counts(_device.ptr(frames_dev), n_groups * gs, h, w, L, R, C, gs,
                                         _device.ptr(counts), _device.ptr(ws), ws_bytes, _lib.WS_ZEROED, stream))
     except Exception:
-        _WORKSPACES.pop((_device.torch().cuda.current_device(), stream), None)
+        _drop_workspace(stream)
         raise
     if global_trees is None:
         total = allreduce_counts(counts, n_groups, group)

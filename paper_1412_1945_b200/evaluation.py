@@ -94,6 +94,7 @@ def classify_confusion(model: BackgroundModel, frames_dev, truth_dev, stats: Eva
     """
     from .detect import _check_frame_shape
     t = _device.torch()
+    frames_dev = _device.frames_on_device(frames_dev)
     n, h, w = int(frames_dev.shape[0]), int(frames_dev.shape[1]), int(frames_dev.shape[2])
     _check_frame_shape(model, h, w)
     want = (n, (h * w + 7) // 8) if packed else (n, h, w)
@@ -102,7 +103,7 @@ def classify_confusion(model: BackgroundModel, frames_dev, truth_dev, stats: Eva
     truth = truth_dev.view(t.uint8) if truth_dev.dtype == t.bool else truth_dev
     if truth.dtype != t.uint8:
         raise ValueError(f"expected a bool or uint8 truth mask, got {truth_dev.dtype}")
-    truth = truth.contiguous()
+    truth = truth.to(frames_dev.device).contiguous()
     cfg = model.config
     counts = t.zeros(4, dtype=t.int64, device=frames_dev.device)
     lib = _lib.load()

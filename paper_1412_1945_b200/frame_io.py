@@ -188,3 +188,32 @@ def save_masks(masks, paths, threads: int = 0) -> None:
         raise ValueError(f"{len(paths)} paths for {n} masks")
     arr, _keep = _paths_array(paths)
     _lib.check(_lib.load().obg_write_pgm_masks(ptr, n, w, h, arr, threads))
+
+
+def write_mask_sequence(directory, masks, names) -> list:
+    """Write masks as PGMs named after the given frame basenames
+    (reference ``frame_io.py:183-192``): ``<stem>.pgm`` per (mask, name) pair,
+    pairs as ``zip`` forms them; returns the written file names.  Runs of
+    same-shaped masks go to the threaded native writer (``save_masks``); the
+    first mask that is not a 2-D bool array raises the reference's
+    ``write_mask_pgm`` ValueError after the masks before it were written."""
+    directory = Path(directory)
+    directory.mkdir(parents=True, exist_ok=True)
+    pairs = list(zip(masks, names))
+    outs = [Path(name).stem + ".pgm" for _, name in pairs]
+    arrays = []
+    for m, _ in pairs:
+        a = np.asarray(m)
+        if a.ndim != 2 or a.dtype != bool:
+            break
+        arrays.append(a)
+    start = 0
+    while start < len(arrays):
+        end = start + 1
+        while end < len(arrays) and arrays[end].shape == arrays[start].shape:
+            end += 1
+        save_masks(np.stack(arrays[start:end]), [directory / o for o in outs[start:end]])
+        start = end
+    if len(arrays) < len(pairs):
+        save_mask(directory / outs[len(arrays)], pairs[len(arrays)][0])   # raises
+    return outs

@@ -16,7 +16,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import _lib
+from . import _device, _lib
 from .errors import FormatError
 from .octree import Octree, decode_tree
 
@@ -196,6 +196,7 @@ def build_presence(frames_dev, levels: int, grid_rows: int = 1, grid_cols: int =
     pyramids ``[n_groups, R*C, PW]`` (int32 words) and optional per-leaf pixel
     counts ``[n_groups, R*C, 8**L]`` in path-code order."""
     from . import _device
+    frames_dev = _device.frames_on_device(frames_dev)
     n, h, w = int(frames_dev.shape[0]), int(frames_dev.shape[1]), int(frames_dev.shape[2])
     n_groups = n // group_size
     n_regions = grid_rows * grid_cols
@@ -211,33 +212,54 @@ def build_presence(frames_dev, levels: int, grid_rows: int = 1, grid_cols: int =
             _device.ptr(frames_dev), n, h, w, levels, grid_rows, grid_cols, group_size, _device.ptr(out),
             _device.ptr(cnt) if cnt is not None else None, _device.ptr(ws), ws_bytes, _lib.WS_ZEROED, stream))
     except Exception:
-        _WORKSPACES.pop((_device.torch().cuda.current_device(), stream), None)   # state unknown: drop it
+        _drop_workspace(stream)
         raise
     return (out, cnt) if counts else out
 
 
 # Build workspaces kept per (device, stream): obg_build_presence hands its
-# workspace back all-zero, so a kept one skips the clearing memset.  Keyed by
-# stream because concurrent builds must not share one.
+# workspace back all-zero, so a kept one skips the clearing memset.  Keyed
+# strictly by stream because concurrent builds must not share one.  Only eager
+# calls use this cache: a CUDA graph holds its workspace's pointer for every
+# replay, so captures get a workspace of their own (passed in explicitly, as
+# pipeline.CapturedStep does, or allocated here and kept alive for the
+# process) -- never one that the cache could replace or drop.
 _WORKSPACES: dict = {}
+_CAPTURE_WORKSPACES: list = []
 
 
-def _workspace(nbytes: int, stream: int):
-    from . import _device
+def new_workspace(nbytes: int):
+    """A zeroed build workspace of ``nbytes`` (owned by the caller)."""
     t = _device.torch()
-    dev = t.cuda.current_device()
+    return t.zeros((max(nbytes, 4) + 3) // 4, dtype=t.int32, device="cuda")
+
+
+def _workspace(nbytes: int, stream: int, explicit=None):
+    t = _device.torch()
+    if explicit is not None:
+        if explicit.numel() * 4 < nbytes or not explicit.is_cuda:
+            raise ValueError(f"workspace must be a CUDA tensor of >= {nbytes} bytes")
+        return explicit
     if t.cuda.is_current_stream_capturing():
-        # graph capture: reuse a workspace created eagerly (warm-up), so the
-        # graph holds no allocation or clearing node for it
-        for (d, _), ws in _WORKSPACES.items():
-            if d == dev and ws.numel() * 4 >= nbytes:
-                return ws
-    key = (dev, stream)
+        ws = new_workspace(nbytes)      # zeroed once at capture; zero-on-return keeps it so
+        _CAPTURE_WORKSPACES.append(ws)
+        return ws
+    key = (t.cuda.current_device(), stream)
     ws = _WORKSPACES.get(key)
     if ws is None or ws.numel() * 4 < nbytes:
-        ws = t.zeros((max(nbytes, 4) + 3) // 4, dtype=t.int32, device="cuda")
+        ws = new_workspace(nbytes)
         _WORKSPACES[key] = ws
     return ws
+
+
+def _drop_workspace(stream: int, explicit=None) -> None:
+    """After a failed launch the workspace state is unknown: drop a cached
+    eager one (an explicit one is re-zeroed)."""
+    t = _device.torch()
+    if explicit is not None:
+        explicit.zero_()
+    elif not t.cuda.is_current_stream_capturing():
+        _WORKSPACES.pop((t.cuda.current_device(), stream), None)
 
 
 def merge_pyramids(pyramids_dev, levels: int, k_min: int, with_cube: bool = False):
@@ -314,10 +336,14 @@ def build_background_model(frames, config: ModelConfig) -> BackgroundModel:
     return build_background_model_device(dev, config, n_groups=n_groups)
 
 
-def build_background_model_device(frames_dev, config: ModelConfig, n_groups: int | None = None) -> BackgroundModel:
+def build_background_model_device(frames_dev, config: ModelConfig, n_groups: int | None = None,
+                                  workspace=None) -> BackgroundModel:
     """Same as :func:`build_background_model` for a CUDA (n, h, w, 3) uint8
-    tensor that already holds the training frames (no host round trip)."""
+    tensor that already holds the training frames (no host round trip).
+    ``workspace``: a caller-owned zeroed buffer (``new_workspace``) of at
+    least ``obg_build_workspace_bytes`` -- what a captured graph should use."""
     from . import _device
+    frames_dev = _device.frames_on_device(frames_dev)
     n, h, w = int(frames_dev.shape[0]), int(frames_dev.shape[1]), int(frames_dev.shape[2])
     if n_groups is None:
         n_groups = min(n, config.training_frames) // config.group_size
@@ -333,14 +359,14 @@ def build_background_model_device(frames_dev, config: ModelConfig, n_groups: int
     cube = _device.empty((n_regions, _lib.cube_words(L)), "int32")
     ws_bytes = lib.obg_build_workspace_bytes(n_groups, n_regions, L)
     stream = _device.stream_handle()
-    ws = _workspace(ws_bytes, stream)
+    ws = _workspace(ws_bytes, stream, workspace)
     try:
         _lib.check(lib.obg_build_model(
             _device.ptr(frames_dev), n_groups * gs, h, w, L, R, C, gs, merge_k_min(n_groups, config.threshold),
             _device.ptr(trees), _device.ptr(merged), _device.ptr(cube), _device.ptr(ws), ws_bytes, _lib.WS_ZEROED,
             stream))
     except Exception:
-        _WORKSPACES.pop((_device.torch().cuda.current_device(), stream), None)
+        _drop_workspace(stream, workspace)
         raise
     return BackgroundModel(config, frame_width=w, frame_height=h, _device_pyramids=merged, _device_cube=cube)
 

@@ -10,15 +10,23 @@ outputs are the static ``model`` / ``masks``.
 
 from __future__ import annotations
 
-from . import _device
+from . import _device, _lib
 from .detect import classify
-from .model import BackgroundModel, ModelConfig, build_background_model_device
+from .model import BackgroundModel, ModelConfig, build_background_model_device, new_workspace
 
 
 class CapturedStep:
     """Build-from-``train`` + classify-``test`` as replayable CUDA graphs: the
     two halves separately (build / classify, for per-phase timing) and the
-    whole step as one graph (step)."""
+    whole step as one graph (step).
+
+    Each graph owns its build workspace (allocated here, referenced for the
+    life of the graph), so a replay never shares scratch with an eager build
+    or with the other graph.  ``build()`` / ``step()`` return a NEW
+    :class:`BackgroundModel` view of the graph's static device buffers, so
+    host views (``trees``, ``to_bytes``, ``write_model``) always read the
+    replay just done; a returned model is valid until its graph replays again.
+    """
 
     def __init__(self, train, test, config: ModelConfig, packed: bool = False, warmup: int = 2):
         t = _device.torch()
@@ -26,28 +34,37 @@ class CapturedStep:
         n, h, w = int(test.shape[0]), int(test.shape[1]), int(test.shape[2])
         shape = (n, (h * w + 7) // 8) if packed else (n, h, w)
         self.masks = t.empty(shape, dtype=t.uint8, device=test.device)
+        n_groups = min(int(train.shape[0]), config.training_frames) // config.group_size
+        ws_bytes = _lib.load().obg_build_workspace_bytes(n_groups, config.grid_rows * config.grid_cols,
+                                                          config.levels)
+        self._ws_build, self._ws_step = new_workspace(ws_bytes), new_workspace(ws_bytes)
         side = t.cuda.Stream()
         side.wait_stream(t.cuda.current_stream())
         with t.cuda.stream(side):          # warm-up: one-time attribute / occupancy setup
             for _ in range(warmup):
-                m = build_background_model_device(train, config)
+                m = build_background_model_device(train, config, workspace=self._ws_build)
                 classify(m, test, out=self.masks, packed=packed)
         t.cuda.current_stream().wait_stream(side)
         t.cuda.synchronize()
         self.build_graph = t.cuda.CUDAGraph()
         with t.cuda.graph(self.build_graph):
-            self.build_model: BackgroundModel = build_background_model_device(train, config)
+            self._build_bufs = build_background_model_device(train, config, workspace=self._ws_build)
         self.classify_graph = t.cuda.CUDAGraph()
         with t.cuda.graph(self.classify_graph):
-            classify(self.build_model, test, out=self.masks, packed=packed)
+            classify(self._build_bufs, test, out=self.masks, packed=packed)
         # the whole step as ONE graph (no launch gap between build and
-        # classify); it owns its own model buffers, step_model
+        # classify); it owns its own model buffers and workspace
         self.step_graph = t.cuda.CUDAGraph()
         with t.cuda.graph(self.step_graph):
-            self.step_model: BackgroundModel = build_background_model_device(train, config)
-            classify(self.step_model, test, out=self.masks, packed=packed)
+            self._step_bufs = build_background_model_device(train, config, workspace=self._ws_step)
+            classify(self._step_bufs, test, out=self.masks, packed=packed)
         t.cuda.synchronize()
-        self._last = self.build_model
+        self._last = self._view(self._build_bufs)
+
+    @staticmethod
+    def _view(bufs: BackgroundModel) -> BackgroundModel:
+        return BackgroundModel(bufs.config, frame_width=bufs.frame_width, frame_height=bufs.frame_height,
+                               _device_pyramids=bufs._dev_pyr, _device_cube=bufs._dev_cube)
 
     @property
     def model(self) -> BackgroundModel:
@@ -56,8 +73,8 @@ class CapturedStep:
 
     def build(self) -> BackgroundModel:
         self.build_graph.replay()
-        self._last = self.build_model
-        return self.build_model
+        self._last = self._view(self._build_bufs)
+        return self._last
 
     def classify(self):
         """Classify with the model of the last build()."""
@@ -67,7 +84,7 @@ class CapturedStep:
     def step(self):
         """Build + classify as one graph replay (model: ``self.model``)."""
         self.step_graph.replay()
-        self._last = self.step_model
+        self._last = self._view(self._step_bufs)
         return self.masks
 
 

@@ -89,12 +89,22 @@ CONFIG_JOBS = [(0, None, "natural"), (1, None, "natural"), (2, None, "natural"),
     [(4, L, v) for v in ("constant", "uniform") for L in (4, 5, 6, 7)]
 
 
+# Extra records appended by ``--extra`` (without regenerating the rest): C4
+# uniform at L7 with threshold 1.0 keeps a leaf only if all 32 training frames
+# hit it -- about half of the 2^21 leaves (each frame hits a leaf with
+# p = 1 - e^-3.96) -- so the merged tree is partial and the 4K test masks are
+# about half foreground: the L7 partial-cell / leaf-mode classify paths are
+# pinned (the thr-0.5 uniform records merge to the full cube, masks all 0).
+EXTRA_JOBS = [(4, 7, "uniform", 1.0)]
+
+
 def config_record(job) -> dict:
     from paper_1412_1945_b200 import scenes
-    cid, levels, variant = job
+    cid, levels, variant = job[:3]
     t0 = time.time()
     sc = scenes.generate(cid, levels=levels, variant=variant)
-    cfg = ref.ModelConfig(levels=sc.config.levels, threshold=sc.config.threshold,
+    threshold = job[3] if len(job) > 3 else sc.config.threshold
+    cfg = ref.ModelConfig(levels=sc.config.levels, threshold=threshold,
                           training_frames=len(sc.train))
     train = list(sc.train)
     model = ref.build_background_model(train, cfg)
@@ -157,7 +167,26 @@ def kat_record() -> dict:
     return kat
 
 
+def main_extra():
+    """Append (or replace) the EXTRA_JOBS records in the existing golden.json."""
+    path = os.path.join(HERE, "golden.json")
+    with open(path) as f:
+        out = json.load(f)
+    for job in EXTRA_JOBS:
+        rec = config_record(job)
+        rec["extra"] = True
+        out["configs"] = [r for r in out["configs"]
+                          if not (r["config"] == rec["config"] and r["variant"] == rec["variant"]
+                                  and r["levels"] == rec["levels"] and r["threshold"] == rec["threshold"])]
+        out["configs"].append(rec)
+    with open(path, "w") as f:
+        json.dump(out, f, indent=0, sort_keys=True)
+    print(f"updated {path}")
+
+
 def main():
+    if "--extra" in sys.argv:
+        return main_extra()
     t0 = time.time()
     out = dict(generator="tests/golden/make_golden.py", reference=getattr(ref, "__version__", "?"),
                numpy=np.__version__)
@@ -166,7 +195,7 @@ def main():
         out["random_cases"] = list(pool.map(random_case_record, range(96)))
     # the 4K stress jobs hold ~4 GB of frames each
     with ProcessPoolExecutor(max_workers=4) as pool:
-        out["configs"] = list(pool.map(config_record, CONFIG_JOBS))
+        out["configs"] = list(pool.map(config_record, CONFIG_JOBS + EXTRA_JOBS))
     path = os.path.join(HERE, "golden.json")
     with open(path, "w") as f:
         json.dump(out, f, indent=0, sort_keys=True)

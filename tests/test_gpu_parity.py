@@ -65,6 +65,26 @@ def test_random_case(cuda, golden, case):
     assert obg.merge_trees(host, cfg.threshold, cfg.levels).to_bytes().hex() == rec["merged"][0][0]
 
 
+@pytest.mark.parametrize("case", range(96))
+def test_loaded_model_detect(cuda, golden, case):
+    """The reference's ``octabg detect`` flow (cli.py:181-187): a model FILE
+    written by the reference -> read_model -> detect_octree per frame (and
+    batched), against the reference's masks.  The trees come from bytes on
+    the host, so the host tree -> obg_leaf_cube -> classify path is pinned."""
+    rec = golden["random_cases"][case]
+    x = random_case_inputs(case)
+    model = obg.read_model(bytes.fromhex(rec["model_file"]))
+    for r in range(rec["grid_rows"]):
+        for c in range(rec["grid_cols"]):
+            assert model.trees[r][c].to_bytes().hex() == rec["merged"][r][c]
+    for probe, want in zip(x["probes"], rec["masks"]):
+        assert mask_hex(obg.detect_octree(model, probe)) == want
+    batch = obg.detect_octree_batch(model, x["probes"])
+    for i, want in enumerate(rec["masks"]):
+        assert mask_hex(batch[i]) == want
+    assert obg.write_model(model).hex() == rec["model_file"]
+
+
 @pytest.mark.parametrize("case", range(0, 96, 7))
 def test_counts(cuda, golden, case):
     rec = golden["random_cases"][case]
@@ -114,8 +134,20 @@ def test_config(cuda, golden, cid):
 def test_config4(cuda, golden, variant, levels):
     from paper_1412_1945_b200 import scenes
     rec = next(r for r in golden["configs"] if r["config"] == 4 and r["variant"] == variant
-               and r["levels"] == levels)
+               and r["levels"] == levels and not r.get("extra"))
     _check_config(rec, scenes.generate(4, levels=levels, variant=variant), cuda)
+
+
+def test_config4_partial_l7(cuda, golden):
+    """C4 uniform 4K at L7 with threshold 1.0 (tests/golden/make_golden.py
+    EXTRA_JOBS): a merged tree with about half of the 2^21 leaves, so the
+    masks are about half foreground and the L7 state table holds mostly
+    partially filled cells -- the thr-0.5 record is a full cube."""
+    from paper_1412_1945_b200 import scenes
+    rec = next(r for r in golden["configs"] if r.get("extra") and r["levels"] == 7 and r["variant"] == "uniform")
+    assert 0.2 < rec["merged_leaves"] / 8 ** 7 < 0.8
+    assert 0.2 < sum(rec["mask_fg"]) / (len(rec["mask_fg"]) * rec["width"] * rec["height"]) < 0.8
+    _check_config(rec, scenes.generate(4, levels=7, variant="uniform"), cuda)
 
 
 # --- reference behaviours (reference tests/test_detect.py, test_model.py) ------------
@@ -337,9 +369,23 @@ def test_captured_step_matches_eager(cuda, golden):
     for _ in range(3):
         masks = step.step().cpu().numpy()
         assert sha(step.model.trees[0][0].to_bytes()) == rec["merged_sha"]
-        step.model._trees = None        # re-materialise from the device after the next replay
         for i in range(len(masks)):
             assert mask_digest(masks[i]) == rec["mask_sha"][i]
+    # different training frames: the model views of the next replays must see
+    # the new trees (no stale host caches), for both graphs
+    old_model = step.model
+    old_bytes = old_model.trees[0][0].to_bytes()
+    half = len(sc.train) // 2
+    alt = np.concatenate([sc.train[half:], sc.test[: len(sc.train) - half]])
+    train.copy_(cuda.from_numpy(alt).cuda())
+    want_alt = orc.to_bytes(orc.build_background_model(list(alt), rec["levels"], rec["threshold"])[(0, 0)])
+    assert want_alt != old_bytes
+    for replay in (step.step, step.build):
+        replay()
+        assert step.model.trees[0][0].to_bytes() == want_alt
+        assert obg.write_model(step.model) == obg.write_model(obg.build_background_model(list(alt), cfg))
+    train.copy_(cuda.from_numpy(sc.train).cuda())
+    step.step()
     # new frames copied into the static input: the replays classify them --
     # the one-graph step and the split build / classify graphs alike
     test.copy_(cuda.from_numpy(sc.train[:24]).cuda())
@@ -401,6 +447,17 @@ def test_build_model_abi_and_workspace_contract(cuda):
         cuda.cuda.synchronize()
         for ws in _WORKSPACES.values():
             assert int(ws.count_nonzero()) == 0
+    # a caller-owned workspace (what a captured graph uses) is handed back zeroed too
+    from paper_1412_1945_b200.model import new_workspace
+    ws = new_workspace(lib.obg_build_workspace_bytes(10, 1, 6))
+    frames = rng.integers(0, 256, size=(10, 48, 64, 3), dtype=np.uint8)
+    cfg = ModelConfig(levels=6, threshold=0.4, training_frames=10)
+    model = obg.build_background_model_device(cuda.from_numpy(frames).cuda(), cfg, workspace=ws)
+    assert model.trees[0][0].to_bytes() == orc.to_bytes(orc.build_background_model(list(frames), 6, 0.4)[(0, 0)])
+    cuda.cuda.synchronize()
+    assert int(ws.count_nonzero()) == 0
+    with pytest.raises(ValueError):
+        obg.build_background_model_device(cuda.from_numpy(frames).cuda(), cfg, workspace=ws[:4])
 
 
 @pytest.mark.gpu
@@ -529,3 +586,31 @@ def test_sharded_build_counts(cuda, levels, grid, gs):
             assert single.trees[r][c].to_bytes() == orc.to_bytes(want[(r, c)]), (r, c)
     probe = frames[3]
     assert np.array_equal(obg.detect_octree(model, probe), orc.detect_octree(want, probe, levels, R, C))
+
+
+def test_device_entry_points_validate_inputs(cuda):
+    """classify / classify_confusion / build_presence / the device build take
+    raw pointers: strided views are made contiguous, host tensors are copied
+    over, malformed shapes / dtypes raise ValueError before any launch."""
+    rng = np.random.default_rng(31)
+    frames = rng.integers(0, 256, size=(6, 24, 40, 3), dtype=np.uint8)
+    cfg = ModelConfig(levels=5, threshold=0.5, training_frames=6)
+    model = obg.build_background_model(list(frames), cfg)
+    dev = cuda.from_numpy(frames).cuda()
+    want = obg.classify(model, dev).cpu()
+    wide = cuda.from_numpy(np.concatenate([frames, frames], axis=2)).cuda()
+    strided = wide[:, :, :40]                      # non-contiguous view of the same pixels
+    assert not strided.is_contiguous()
+    assert cuda.equal(obg.classify(model, strided).cpu(), want)
+    assert cuda.equal(obg.classify(model, cuda.from_numpy(frames)).cpu(), want)   # CPU tensor in
+    assert cuda.equal(obg.build_presence(strided, 5), obg.build_presence(dev, 5))
+    m2 = obg.build_background_model_device(strided, cfg)
+    assert m2.trees[0][0] == model.trees[0][0]
+    for bad in (dev[..., :2], dev.to(cuda.int16), dev[0]):
+        with pytest.raises(ValueError):
+            obg.classify(model, bad)
+        with pytest.raises(ValueError):
+            obg.build_presence(bad, 5)
+    truth = cuda.zeros((6, 24, 40), dtype=cuda.uint8)
+    st = obg.classify_confusion(model, strided, truth)
+    assert st.false_pos == int(want.sum())

@@ -272,3 +272,64 @@ def test_native_decode_tree_matches_python_walk():
             except FormatError as e:
                 results.append(("err", str(e), e.offset))
         assert results[0] == results[1], (case, results)
+
+
+def test_store_code_masks_digits_like_reference():
+    """Reference store_code/contains_code walk ``(code >> shift) & 7``
+    (octree.py:158-191): only the low 3*depth bits select the path, for
+    negative and oversized codes alike; a call never half-mutates the tree."""
+    t = Octree(3)
+    t.store_code(-1)
+    assert t.leaf_codes() == [511] and t.to_bytes().hex() == "80808000"
+    t = Octree(3)
+    t.store_code(8 ** 3 + 5)
+    assert t.leaf_codes() == [5] and t.contains_code(5) and t.contains_code(8 ** 3 + 5)
+    assert t.node_count == 4 and not t.contains_code(6)
+
+
+def test_root_assignment():
+    """``tree.root = other.root`` / ``= None`` (the reference assigns
+    ``merged.root = root``, model.py:136)."""
+    a = Octree(3)
+    for c in ((0, 0, 0), (255, 0, 128), (9, 200, 77)):
+        a.store(c)
+    b = Octree(3)
+    b.root = a.root
+    assert b == a and b.to_bytes() == a.to_bytes()
+    b.root = None
+    assert b.is_empty and b.to_bytes() == b"" and b.node_count == 0
+    # a subtree view: the level-1 child of a's first colour, re-rooted
+    sub = next(ch for ch in a.root.children if ch is not None)
+    c = Octree(2)
+    c.root = sub
+    assert c.leaf_codes() == sorted({code & 63 for code in a.leaf_codes() if code >> 6 == sub._prefix})
+    # any object with a ``children`` list of 8 (e.g. the reference's _Node)
+    class N:
+        def __init__(self, kids=None):
+            self.children = kids or [None] * 8
+    leaf = N()
+    d = Octree(2)
+    d.root = N([None, N([leaf] + [None] * 7)] + [None] * 6)
+    assert d.leaf_codes() == [8] and d.node_count == 3
+
+
+def test_sparse_tree_ops_are_cheap():
+    """O(nodes) host trees: a 2-colour depth-8 round trip well under the
+    reference property test's 200 ms deadline (tests/test_octree.py:238-247)."""
+    import time
+    t0 = time.perf_counter()
+    for _ in range(20):
+        t = Octree(8)
+        t.store((255, 255, 255))
+        t.store((1, 2, 3))
+        data = t.to_bytes()
+        r = Octree.from_bytes(data, 8)
+        assert r == t and r.to_bytes() == data and r.node_count == 17
+    assert (time.perf_counter() - t0) / 20 < 0.02
+
+
+def test_frames_validation_without_gpu():
+    from paper_1412_1945_b200 import _device
+    for bad in (np.zeros((2, 4, 4), np.uint8), np.zeros((2, 4, 4, 4), np.uint8), np.zeros((2, 4, 4, 3), np.int16)):
+        with pytest.raises(ValueError):
+            _device.frames_on_device(bad)
