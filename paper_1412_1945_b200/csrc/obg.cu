@@ -21,6 +21,7 @@
 #include <stdio.h>
 #include <string.h>
 #include <stdarg.h>
+#include <type_traits>
 
 #include "../../include/obg.h"
 
@@ -624,6 +625,14 @@ __device__ __forceinline__ uint32_t lds_at(uint32_t off) {
 }
 __device__ __forceinline__ void reds_or_at(uint32_t off, uint32_t v) {
   asm volatile("red.shared.or.b32 [%0+1024], %1;" :: "r"(off), "r"(v) : "memory");
+}
+// ld.shared at [off] only where `skip` is 0; 0xFFFFFFFF (all present)
+// elsewhere: a predicated-off lane adds no bank access to the wavefront
+__device__ __forceinline__ uint32_t lds_at_unless(uint32_t off, uint32_t skip) {
+  uint32_t v = 0xFFFFFFFFu;
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %2, 0;\n\t@p ld.shared.u32 %0, [%1+1024];\n\t}"
+               : "+r"(v) : "r"(off), "r"(skip));
+  return v;
 }
 // red.shared.or at [off] only in the lanes where `hit` is 0 (a predicated ATOMS)
 __device__ __forceinline__ void reds_or_if(uint32_t off, uint32_t v, uint32_t hit) {
@@ -1247,8 +1256,10 @@ __device__ __forceinline__ uint32_t build_unit_l7h(const uint32_t (&w)[12], uint
     l7h_pair_dyn<0>(w, g / 2 + 1, hmask, addr[2], bsel[2], mis[2], addr[3], bsel[3], mis[3]);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const uint32_t wd = lds_at(addr[j]);
-      v[j] = __funnelshift_r(wd, wd, bsel[j]) | mis[j];                  // other half: a hit
+      // pixels of the other half are hits and do not touch shared memory
+      // (uniform-random frames: half the lookups, fewer bank conflicts)
+      const uint32_t wd = lds_at_unless(addr[j], mis[j] & 1u);
+      v[j] = __funnelshift_r(wd, wd, bsel[j]) | mis[j];
     }
     const bool miss = valid && !(v[0] & v[1] & v[2] & v[3] & 1u);
     if (__any_sync(0xFFFFFFFFu, miss)) {
@@ -2249,43 +2260,84 @@ __device__ __forceinline__ uint32_t l7_leaf_word_if(const char* __restrict__ cub
                : "+r"(wd) : "l"(cube + off), "r"(pred));
   return __funnelshift_r(wd, wd, x >> 17);
 }
+// compile-time loop over the 16 pixels of a unit: f(std::integral_constant<int, J>)
+template <int J = 0, class F>
+__device__ __forceinline__ void for16(F&& f) {
+  if constexpr (J < 16) {
+    f(std::integral_constant<int, J>{});
+    for16<J + 1>(f);
+  }
+}
+
+// 16 background bits (bit j = pixel j's leaf present) -> the unit's output
+template <int OUT>
+__device__ __forceinline__ void emit_bits(uint32_t bg, uint8_t* out, int64_t u, ConfAcc& acc) {
+  const uint32_t fg = ~bg & 0xFFFFu;
+  if constexpr (OUT == OUT_U8) {
+    uint4 o;                                    // nibble -> four 0/1 bytes: n * 0x00204081 & 0x01010101
+    o.x = ((fg & 15u) * 0x00204081u) & 0x01010101u;
+    o.y = (((fg >> 4) & 15u) * 0x00204081u) & 0x01010101u;
+    o.z = (((fg >> 8) & 15u) * 0x00204081u) & 0x01010101u;
+    o.w = ((fg >> 12) * 0x00204081u) & 0x01010101u;
+    __stcs(reinterpret_cast<uint4*>(out) + u, o);
+  } else if constexpr (OUT == OUT_PACKED) {
+    reinterpret_cast<uint16_t*>(out)[u] = uint16_t(fg);
+  } else {
+    uint32_t t;
+    if constexpr (OUT == OUT_CONF_U8) {
+      const uint4 q = __ldcs(reinterpret_cast<const uint4*>(out) + u);
+      t = nz_nibble(q.x) | (nz_nibble(q.y) << 4) | (nz_nibble(q.z) << 8) | (nz_nibble(q.w) << 12);
+    } else {
+      t = __ldcs(reinterpret_cast<const uint16_t*>(out) + u);
+    }
+    acc.add(fg, t, 0xFFFFu);
+  }
+}
+
+// One 16-pixel unit at L = 7.  The per-pixel results are kept as BITS of
+// three registers (some / all / background) and every pixel's [*, G, B, R]
+// operand is re-extracted from the unit's words where it is used, so the
+// live set is the two units of the double buffer plus a handful of words:
+// no local-memory spills at the 64-register cap of 2 x 512 threads per SM
+// (the earlier px[16] / v[16] arrays spilled 136-228 bytes per thread).
 template <int OUT>
 __device__ __forceinline__ void classify_unit_l7(const uint32_t (&w)[12], const uint32_t* s_state,
                                                  const uint32_t* __restrict__ cube, uint8_t* mask, int64_t u,
                                                  ConfAcc& acc, int& leaf_run) {
-  uint32_t px[16], v[16];
-  unpack16<0, 6>(w, px);                                            // [*, G, B, R] operands
+  const char* cb = reinterpret_cast<const char*>(cube);
+  uint32_t bg = 0;
   if (leaf_run > 0) {
     --leaf_run;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = l7_leaf_word(reinterpret_cast<const char*>(cube), px[j]);
-    emit16<OUT>(v, mask, u, acc);
+    for16([&](auto jc) {
+      constexpr int j = decltype(jc)::value;
+      bg |= (l7_leaf_word(cb, pixel_word_gbr<j>(w)) & 1u) << j;
+    });
+    emit_bits<OUT>(bg, mask, u, acc);
     return;
   }
-  uint32_t mixed = 0;
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    v[j] = s7_state(s_state, px[j]);
-    mixed |= (v[j] ^ (v[j] >> 1)) & 1u;                             // some but not all leaves
-  }
-  const uint32_t bal = __ballot_sync(__activemask(), mixed);
+  uint32_t some = 0, all = 0;
+  for16([&](auto jc) {
+    constexpr int j = decltype(jc)::value;
+    const uint32_t st = s7_state(s_state, pixel_word_gbr<j>(w));
+    some |= (st & 1u) << j;
+    all |= ((st >> 1) & 1u) << j;
+  });
+  const uint32_t mixed = some & ~all;                               // some but not all leaves
+  bg = all;
+  const uint32_t bal = __ballot_sync(__activemask(), mixed != 0u);
   if (bal) {
-    // branch-free: pixels in partially filled cells read their leaf word
-    // (predicated loads: no traffic for the others)
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const uint32_t mj = (v[j] ^ (v[j] >> 1)) & 1u;
-      v[j] = mj ? l7_leaf_word_if(reinterpret_cast<const char*>(cube), px[j], mj) : (v[j] >> 1);
-    }
+    // pixels in partially filled cells read their leaf word (predicated
+    // loads: no traffic for the others)
+    for16([&](auto jc) {
+      constexpr int j = decltype(jc)::value;
+      bg |= (l7_leaf_word_if(cb, pixel_word_gbr<j>(w), (mixed >> j) & 1u) & 1u) << j;
+    });
     // leaf mode only where partial cells are common (several lanes met one):
     // with sparse partial cells (e.g. uniform-random frames and a nearly
     // full model) the state table answers almost every pixel
     if (__popc(bal) >= L7_LEAF_LANES) leaf_run = L7_LEAF_RUN;
-  } else {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] >>= 1;                        // all children present
   }
-  emit16<OUT>(v, mask, u, acc);
+  emit_bits<OUT>(bg, mask, u, acc);
 }
 
 template <int OUT>

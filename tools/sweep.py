@@ -36,11 +36,11 @@ def main():
         md.write("| workload | step ms | value Mpx/s | build ms | classify ms | classify frac | build frac | parity |\n")
         md.write("|---|---|---|---|---|---|---|---|\n")
         for name, d in rows:
-            c = d["config"]
+            c, ph = d["config"], d["phases"]
             par = d.get("parity") or {}
             ok = all(v for k, v in par.items() if k != "frames") if par else None
             md.write(f"| {name}: {c['workload'].split(':')[0]} | {d['ms_per_step']} | {d['value']:,.0f} | "
-                     f"{c['build_ms']} | {c['classify_ms']} | {d['roofline']['frac']} | {c['build_hbm_frac']} | "
+                     f"{ph['build_ms']} | {ph['classify_ms']} | {d['roofline']['frac']} | {ph['build_hbm_frac']} | "
                      f"{ok} |\n")
 
 
