@@ -344,22 +344,37 @@ __device__ __forceinline__ uint32_t rgb_word_scalar(const uint8_t* p) {
 // (and those of a second unit) issued back to back: left to itself ptxas sinks
 // them next to their first use to save registers, which starves the memory
 // pipe (ncu r2: long-scoreboard stalls dominated classify).
+// OBG_LOAD_POLICY 1: frame loads carry an L2 evict-first policy and skip L1
+// (every frame byte is read once), so the streams do not push the small
+// L2-resident operands (build workspace, L7 classify cube) out of L2.
+#ifndef OBG_LOAD_POLICY
+#define OBG_LOAD_POLICY 0
+#endif
+#if OBG_LOAD_POLICY
+__device__ __forceinline__ uint64_t frame_policy() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+#define OBG_LDV4(W0, W1, W2, W3, P, OFF)                                                               \
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4+" #OFF "], %5;" \
+               : "=r"(W0), "=r"(W1), "=r"(W2), "=r"(W3) : "l"(P), "l"(frame_policy()))
+#else
+#define OBG_LDV4(W0, W1, W2, W3, P, OFF)                                        \
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4+" #OFF "];"            \
+               : "=r"(W0), "=r"(W1), "=r"(W2), "=r"(W3) : "l"(P))
+#endif
 __device__ __forceinline__ void load_unit_at(const uint8_t* p, uint32_t (&w)[12]) {
-  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "l"(p));
-  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4+16];"
-               : "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]) : "l"(p));
-  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4+32];"
-               : "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]) : "l"(p));
+  OBG_LDV4(w[0], w[1], w[2], w[3], p, 0);
+  OBG_LDV4(w[4], w[5], w[6], w[7], p, 16);
+  OBG_LDV4(w[8], w[9], w[10], w[11], p, 32);
 }
 __device__ __forceinline__ void load_unit(const uint8_t* __restrict__ base, int64_t u, uint32_t (&w)[12]) {
-  const uint8_t* p = base + 48 * u;
-  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "l"(p));
-  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4+16];"
-               : "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]) : "l"(p));
-  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4+32];"
-               : "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]) : "l"(p));
+  load_unit_at(base + 48 * u, w);
+}
+// one lane's bulk prefetch of `bytes` (multiple of 16, 16-aligned) into L2
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -823,6 +838,9 @@ __device__ __forceinline__ void flush_segment(uint32_t* s_bits, uint32_t* dst, i
   __syncthreads();                                   // bitset clear before the next segment
 }
 
+#ifndef OBG_BUILD_PF
+#define OBG_BUILD_PF 0            // > 0: lane 0 bulk-prefetches the warp's chunk this many iterations ahead into L2
+#endif
 template <int L, bool SMEM_BITS, bool COUNTS>
 __global__ void __launch_bounds__(BUILD_BLOCK, OBG_BUILD_MINB)
 k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t total_units,
@@ -872,6 +890,8 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
     const uint8_t* fp = frames + 48 * (u + rel0 + lane);
 #define OBG_BUILD_STEP(CUR, NXT)                                                              \
     {                                                                                          \
+      if (OBG_BUILD_PF > 0 && lane == 0 && k + OBG_BUILD_PF < n_full)                          \
+        prefetch_l2_bulk(fp + OBG_BUILD_PF * STEP, 48 * 32);                                   \
       if (k + STAGES - 1 < n_lane) load_unit_at(fp + (STAGES - 1) * STEP, NXT);                \
       if (k < n_full) build_unit<L, SMEM_BITS, COUNTS, true>(CUR, bits, cnt, true);            \
       else build_unit<L, SMEM_BITS, COUNTS, false>(CUR, bits, cnt, k < n_lane);                \
@@ -2543,34 +2563,79 @@ __global__ void k_pack_codes(const uint8_t* __restrict__ px, int64_t n, int L, u
 //   pos = sum_{m<l} (rank_m(p >> 3(l-m)) + 1) + sum_{m>=l} rank_m(p << 3(m-l))
 // where rank_m(q) = number of level-m nodes with code < q.  Node (l, p) emits
 // byte p of level l+1 (its child mask), leaves emit 0 (octree.py:258-267).
-__global__ void k_scan_pyramid(const uint32_t* __restrict__ pyr, int L, uint32_t* __restrict__ prefix,
-                               uint32_t* __restrict__ total) {
-  // single CTA (1024 threads): exclusive popcount prefix per level
-  __shared__ uint32_t s_sum[1024];
-  __shared__ uint32_t s_carry;
-  for (int l = 1; l <= L; ++l) {
-    const int64_t off = level_offset(l), nw = level_words(l);
-    if (threadIdx.x == 0) s_carry = 0;
-    __syncthreads();
-    for (int64_t base = 0; base < nw; base += 1024) {
-      const int64_t i = base + threadIdx.x;
-      const uint32_t c = i < nw ? __popc(pyr[off + i]) : 0u;
-      s_sum[threadIdx.x] = c;
-      __syncthreads();
-      for (int d = 1; d < 1024; d <<= 1) {
-        uint32_t t = threadIdx.x >= d ? s_sum[threadIdx.x - d] : 0u;
-        __syncthreads();
-        s_sum[threadIdx.x] += t;
-        __syncthreads();
-      }
-      if (i < nw) prefix[off + i] = s_carry + s_sum[threadIdx.x] - c;
-      __syncthreads();
-      if (threadIdx.x == 1023) s_carry += s_sum[1023];
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) total[l] = s_carry;
-    __syncthreads();
+// Exclusive popcount prefix over ALL words of the pyramid (levels
+// concatenated), prefix[PW] = the node count, in two multi-CTA launches:
+// per-chunk totals, then each CTA adds the totals of the chunks before it and
+// scans its own chunk.  A level's local rank is prefix[off + w] - prefix[off].
+constexpr int SCAN_BLOCK = 1024;
+constexpr int SCAN_CHUNK = 4 * SCAN_BLOCK;       // words per CTA (4 per thread)
+
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s_warp, uint32_t& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, x, d);
+    if (lane >= d) x += t;
   }
+  if (lane == 31) s_warp[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t y = lane < SCAN_BLOCK / 32 ? s_warp[lane] : 0u;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, y, d);
+      if (lane >= d) y += t;
+    }
+    s_warp[lane] = y;                                  // inclusive warp totals
+  }
+  __syncthreads();
+  total = s_warp[SCAN_BLOCK / 32 - 1];
+  const uint32_t before = wid ? s_warp[wid - 1] : 0u;
+  __syncthreads();
+  return before + x - v;
+}
+
+__global__ void __launch_bounds__(SCAN_BLOCK)
+k_scan_partials(const uint32_t* __restrict__ pyr, int64_t PW, uint32_t* __restrict__ partials) {
+  __shared__ uint32_t s_warp[32];
+  const int64_t base = int64_t(blockIdx.x) * SCAN_CHUNK + 4 * threadIdx.x;
+  uint32_t c = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) c += base + k < PW ? __popc(pyr[base + k]) : 0u;
+  uint32_t total;
+  block_exclusive_scan(c, s_warp, total);
+  if (threadIdx.x == 0) partials[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(SCAN_BLOCK)
+k_scan_finish(const uint32_t* __restrict__ pyr, int64_t PW, const uint32_t* __restrict__ partials,
+              uint32_t* __restrict__ prefix) {
+  __shared__ uint32_t s_warp[32];
+  __shared__ uint32_t s_carry;
+  if (threadIdx.x < 32) {
+    uint32_t c = 0;
+    for (uint32_t b = threadIdx.x; b < blockIdx.x; b += 32) c += partials[b];
+    c = __reduce_add_sync(0xFFFFFFFFu, c);
+    if (threadIdx.x == 0) s_carry = c;
+  }
+  const int64_t base = int64_t(blockIdx.x) * SCAN_CHUNK + 4 * threadIdx.x;
+  uint32_t pc[4], c = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    pc[k] = base + k < PW ? __popc(pyr[base + k]) : 0u;
+    c += pc[k];
+  }
+  uint32_t total;
+  uint32_t run = block_exclusive_scan(c, s_warp, total) + s_carry;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (base + k < PW) prefix[base + k] = run;
+    run += pc[k];
+  }
+  if (base <= PW && PW < base + 4) prefix[PW] = s_carry + total;   // the CTA holding the end writes the node count
+  if (PW == int64_t(gridDim.x) * SCAN_CHUNK && blockIdx.x == gridDim.x - 1 && threadIdx.x == SCAN_BLOCK - 1)
+    prefix[PW] = s_carry + total;
 }
 
 __device__ __forceinline__ uint32_t rank_of(const uint32_t* __restrict__ pyr, const uint32_t* __restrict__ prefix,
@@ -2579,31 +2644,33 @@ __device__ __forceinline__ uint32_t rank_of(const uint32_t* __restrict__ pyr, co
   const uint64_t w = q >> 5;
   const uint32_t b = uint32_t(q & 31u);
   const uint32_t word = pyr[off + w];
-  return prefix[off + w] + __popc(b ? (word & ((1u << b) - 1u)) : 0u);
+  return prefix[off + w] - __ldg(prefix + off) + __popc(b ? (word & ((1u << b) - 1u)) : 0u);
 }
 
-__global__ void k_serialize(const uint32_t* __restrict__ pyr, const uint32_t* __restrict__ prefix, int L,
-                            uint8_t* __restrict__ out) {
+// One thread per (pyramid word, bit): a warp shares one word, so the level
+// search and the word load are warp-uniform, and each node's L rank lookups
+// are independent loads (ILP) instead of a per-word serial loop over its bits.
+__global__ void __launch_bounds__(256)
+k_serialize(const uint32_t* __restrict__ pyr, const uint32_t* __restrict__ prefix, int L, uint8_t* __restrict__ out) {
   const int64_t PW = pyr_words(L);
-  for (int64_t gw = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; gw < PW; gw += int64_t(gridDim.x) * blockDim.x) {
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < PW * 32; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t gw = t >> 5;
+    const int b = int(t & 31);
+    const uint32_t word = __ldg(pyr + gw);
+    if (!((word >> b) & 1u)) continue;
     int l = 1;
     while (l < L && gw >= level_offset(l + 1)) ++l;
     const int64_t w = gw - level_offset(l);
-    uint32_t word = pyr[gw];
-    while (word) {
-      const int b = __ffs(word) - 1;
-      word &= word - 1u;
-      const uint64_t p = uint64_t(w) * 32 + b;
-      uint64_t pos = 1;  // the root precedes every node
-      for (int m = 1; m < l; ++m) pos += rank_of(pyr, prefix, m, p >> (3 * (l - m))) + 1;
-      for (int m = l; m <= L; ++m) pos += rank_of(pyr, prefix, m, p << (3 * (m - l)));
-      uint8_t byte = 0;
-      if (l < L) {
-        const uint32_t cw = pyr[level_offset(l + 1) + (p >> 2)];
-        byte = uint8_t(cw >> (8 * (p & 3)));
-      }
-      out[pos] = byte;
+    const uint64_t p = uint64_t(w) * 32 + uint64_t(b);
+    uint64_t pos = 1;  // the root precedes every node
+    for (int m = 1; m < l; ++m) pos += rank_of(pyr, prefix, m, p >> (3 * (l - m))) + 1;
+    for (int m = l; m <= L; ++m) pos += rank_of(pyr, prefix, m, p << (3 * (m - l)));
+    uint8_t byte = 0;
+    if (l < L) {
+      const uint32_t cw = __ldg(pyr + level_offset(l + 1) + (p >> 2));
+      byte = uint8_t(cw >> (8 * (p & 3)));
     }
+    out[pos] = byte;
   }
 }
 
@@ -2848,6 +2915,183 @@ static int launch_build_flat(const uint8_t* frames, int64_t units_per_frame, int
   return OBG_OK;
 }
 
+// ---------------------------------------------------------------------------
+// a13: per-leaf pixel occupancy counts (the optional out_counts of
+// obg_build_presence, the restatement np.bincount of
+// pack_codes per frame tree, reference model.py:107 / tests/test_model.py:22-26).
+// A separate streaming pass, so counts never slow the presence build.  The
+// CTA streams a contiguous unit range (tree segments as K1); per pixel the
+// warp aggregates equal bins with __match_any_sync and the lowest peer adds
+// the peer count:
+//   L <= 5: into a histogram privatised per CTA in shared memory (8^L u32,
+//           cube order, 128 KB at L = 5), flushed to the tree's path-order
+//           counts in HBM (global atomics, non-zero bins only) at each
+//           segment end;
+//   L >= 6: straight into the tree's counts in global memory (1 MB at L = 6
+//           does not fit shared memory; the warp aggregation is what keeps a
+//           single-colour hot spot cheap).
+// ---------------------------------------------------------------------------
+constexpr int HIST_BLOCK = 1024;
+#ifndef OBG_HIST_AGG
+#define OBG_HIST_AGG 0            // 1: __match_any_sync aggregation everywhere (measured, slower)
+#endif
+
+// add `cnt` at bin `key` (all lanes call it together; `go` = lane has an add):
+// shared memory -- plain atomics (the shared atomic unit merges equal
+// addresses of a warp itself); global -- one warp-reduced add when every
+// lane adds to the same bin (a single-colour hot spot), else per lane
+template <bool SMEM>
+__device__ __forceinline__ void hist_add(uint32_t* at, uint32_t key, uint32_t cnt, bool go, int lane) {
+  if constexpr (SMEM) {
+    if (go) atomicAdd(at, cnt);
+  } else {
+    const uint32_t k0 = __shfl_sync(0xFFFFFFFFu, key, 0);
+    if (__all_sync(0xFFFFFFFFu, go && key == k0)) {
+      const uint32_t sum = __reduce_add_sync(0xFFFFFFFFu, cnt);
+      if (lane == 0) atomicAdd(at, sum);
+    } else if (go) {
+      atomicAdd(at, cnt);
+    }
+  }
+}
+
+template <int L, bool SMEM>
+__device__ __forceinline__ void hist_unit(const uint32_t (&w)[12], bool valid, uint32_t* dst, int lane) {
+#if OBG_HIST_AGG == 1
+  // __match_any_sync warp aggregation of equal bins (the lowest peer adds the
+  // peer count).  Measured and NOT the default: MATCH.ANY per pixel costs ~5x
+  // on mixed warps (C4 uniform L5: 2.05 ms vs 0.35 ms for presence + counts)
+  // and the shared atomic unit already merges a warp's equal addresses.
+  for16([&](auto jc) {
+    constexpr int j = decltype(jc)::value;
+    const uint32_t idx = cube_idx<L>(pixel_word<j>(w));
+    const uint32_t key = valid ? idx : 0xFFFFFFFFu;
+    const uint32_t peers = __match_any_sync(0xFFFFFFFFu, key);
+    if (valid && lane == __ffs(peers) - 1) atomicAdd(dst + (SMEM ? idx : cube_to_code(idx, L)), uint32_t(__popc(peers)));
+  });
+#else
+  if constexpr (SMEM) {
+    // privatised shared histogram: one plain shared atomic per pixel (A/B,
+    // tools/ab.py: fastest on every scene incl. the single-colour hot spot)
+    for16([&](auto jc) {
+      constexpr int j = decltype(jc)::value;
+      if (valid) atomicAdd(dst + cube_idx<L>(pixel_word<j>(w)), 1u);
+    });
+  } else {
+    // global counts: run-length over the thread's 16 consecutive pixels (one
+    // add per run of equal bins), and one warp-reduced add when all lanes
+    // add to the same bin -- a single-colour frame would otherwise serialise
+    // 32 same-address global atomics per instruction (C4 constant L6:
+    // 10.4 ms -> 0.54 ms)
+    uint32_t prev = 0, run = 0;
+    for16([&](auto jc) {
+      constexpr int j = decltype(jc)::value;
+      const uint32_t pos = cube_to_code(cube_idx<L>(pixel_word<j>(w)), L);
+      if constexpr (j == 0) {
+        prev = pos;
+        run = 1;
+      } else {
+        const bool change = pos != prev;
+        hist_add<SMEM>(dst + prev, prev, run, valid && change, lane);
+        run = change ? 1u : run + 1u;
+        prev = pos;
+      }
+    });
+    hist_add<SMEM>(dst + prev, prev, run, valid, lane);
+  }
+#endif
+}
+
+template <int L, bool SMEM>
+__global__ void __launch_bounds__(HIST_BLOCK, 1)
+k_hist(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t total_units, int group_size,
+       int64_t units_per_cta, uint32_t* __restrict__ counts) {
+  extern __shared__ __align__(16) uint32_t s_hist[];
+  constexpr uint32_t NB = 1u << (3 * L);
+  const int64_t u_begin = int64_t(blockIdx.x) * units_per_cta;
+  const int64_t u_end = min(total_units, u_begin + units_per_cta);
+  if (u_begin >= u_end) return;
+  if constexpr (SMEM) {
+    for (uint32_t i = threadIdx.x; i < NB; i += HIST_BLOCK) s_hist[i] = 0u;
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & 31;
+  const int64_t upt = units_per_frame * group_size;
+  int64_t u = u_begin;
+  while (u < u_end) {
+    const int64_t tree = u / upt;
+    const int64_t seg_end = min(u_end, (tree + 1) * upt);
+    uint32_t* dst = counts + tree * int64_t(NB);
+    const int64_t seg_len = seg_end - u;
+    const int32_t rel0 = int32_t(threadIdx.x) - lane;
+    const int32_t n_it = seg_len > rel0 ? int32_t((seg_len - rel0 + HIST_BLOCK - 1) / HIST_BLOCK) : 0;
+    const int32_t n_lane = seg_len > rel0 + lane ? int32_t((seg_len - rel0 - lane + HIST_BLOCK - 1) / HIST_BLOCK) : 0;
+    constexpr int64_t STEP = 48 * int64_t(HIST_BLOCK);
+    const uint8_t* fp = frames + 48 * (u + rel0 + lane);
+    uint32_t* hdst = SMEM ? s_hist : dst;
+    uint32_t wa[12], wb[12];
+    if (0 < n_lane) load_unit_at(fp, wa);
+    for (int32_t k = 0; k < n_it;) {
+      if (k + 1 < n_lane) load_unit_at(fp + STEP, wb);
+      hist_unit<L, SMEM>(wa, k < n_lane, hdst, lane);
+      fp += STEP;
+      if (++k >= n_it) break;
+      if (k + 1 < n_lane) load_unit_at(fp + STEP, wa);
+      hist_unit<L, SMEM>(wb, k < n_lane, hdst, lane);
+      fp += STEP;
+      ++k;
+    }
+    if constexpr (SMEM) {
+      __syncthreads();
+      for (uint32_t i = threadIdx.x; i < NB; i += HIST_BLOCK) {
+        const uint32_t c = s_hist[i];
+        if (c) {
+          atomicAdd(dst + cube_to_code(i, L), c);
+          s_hist[i] = 0u;
+        }
+      }
+      __syncthreads();
+    }
+    u = seg_end;
+  }
+}
+
+template <int L>
+static int launch_hist(const uint8_t* frames, int64_t units_per_frame, int64_t total_units, int group_size,
+                       uint32_t* counts, cudaStream_t st) {
+  constexpr bool SMEM = L <= 5;
+  const size_t smem = SMEM ? (size_t(1) << (3 * L)) * 4 : 0;
+  static DevCache attr;
+  if (!attr()) {
+    if (smem > 48 * 1024)
+      CUDA_TRY(cudaFuncSetAttribute(k_hist<L, SMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr() = occupancy(k_hist<L, SMEM>, HIST_BLOCK, smem);
+  }
+  const int64_t max_ctas = int64_t(sm_count()) * attr();
+  int64_t per_cta = (total_units + max_ctas - 1) / max_ctas;
+  if (per_cta < int64_t(HIST_BLOCK) * 4) per_cta = int64_t(HIST_BLOCK) * 4;
+  if (per_cta >= (int64_t(1) << 31) - 2 * HIST_BLOCK)
+    return set_err(OBG_EUNSUPPORTED, "too many pixels per launch (%lld units per CTA)", (long long)per_cta);
+  const int grid = int((total_units + per_cta - 1) / per_cta);
+  k_hist<L, SMEM><<<grid, HIST_BLOCK, smem, st>>>(frames, units_per_frame, total_units, group_size, per_cta, counts);
+  LAUNCH_CHECK("k_hist");
+  return OBG_OK;
+}
+
+static int launch_hist_any(int L, const uint8_t* frames, int64_t upf, int64_t total_units, int group_size,
+                           uint32_t* counts, cudaStream_t st) {
+  switch (L) {
+    case 1: return launch_hist<1>(frames, upf, total_units, group_size, counts, st);
+    case 2: return launch_hist<2>(frames, upf, total_units, group_size, counts, st);
+    case 3: return launch_hist<3>(frames, upf, total_units, group_size, counts, st);
+    case 4: return launch_hist<4>(frames, upf, total_units, group_size, counts, st);
+    case 5: return launch_hist<5>(frames, upf, total_units, group_size, counts, st);
+    case 6: return launch_hist<6>(frames, upf, total_units, group_size, counts, st);
+    case 7: return launch_hist<7>(frames, upf, total_units, group_size, counts, st);
+    default: return launch_hist<8>(frames, upf, total_units, group_size, counts, st);
+  }
+}
+
 static int launch_build_l7h(const uint8_t* frames, int64_t units_per_frame, int64_t total_units, int group_size,
                             uint32_t* ws, uint32_t* out_pyr, int64_t n_trees, uint32_t* zero_cube, int64_t zero_words,
                             cudaStream_t st) {
@@ -2927,6 +3171,13 @@ static int build_presence_impl(const uint8_t* frames, int n_frames, int height, 
   if (!(flags & OBG_WS_ZEROED)) CUDA_TRY(cudaMemsetAsync(ws, 0, size_t(n_trees * ws_words(levels) * 4), st));
   if (out_counts) CUDA_TRY(cudaMemsetAsync(out_counts, 0, size_t(n_trees) * (size_t(1) << (3 * levels)) * 4, st));
   int rc = OBG_OK;
+  if (flat && out_counts) {
+    // presence through the fast kernels, counts in their own streaming pass
+    const int64_t upf = P / 16, total_units = used_pixels / 16;
+    rc = launch_hist_any(levels, frames, upf, total_units, group_size, out_counts, st);
+    if (rc != OBG_OK) return rc;
+    out_counts = nullptr;
+  }
   if (flat) {
     const int64_t upf = P / 16, total_units = used_pixels / 16;
     switch (levels) {
@@ -3234,7 +3485,8 @@ int obg_classify_confusion(const uint8_t* frames, int n_frames, int height, int 
 
 int64_t obg_serialize_workspace_bytes(int levels) {
   if (levels < 1 || levels > 8) return -1;
-  return (pyr_words(levels) + 16) * 4;
+  const int64_t PW = pyr_words(levels);
+  return (PW + 1 + (PW + SCAN_CHUNK - 1) / SCAN_CHUNK + 16) * 4;     // prefix (+ node count), chunk totals
 }
 
 int obg_serialize(const uint32_t* pyramid, int levels, int has_root, uint8_t* out, int64_t out_capacity,
@@ -3245,16 +3497,18 @@ int obg_serialize(const uint32_t* pyramid, int levels, int has_root, uint8_t* ou
   if (workspace_bytes < obg_serialize_workspace_bytes(levels) || !workspace)
     return set_err(OBG_EINVAL, "workspace too small");
   cudaStream_t st = as_stream(stream);
+  const int64_t PW = pyr_words(levels);
   uint32_t* prefix = static_cast<uint32_t*>(workspace);
-  uint32_t* totals = prefix + pyr_words(levels);
-  CUDA_TRY(cudaMemsetAsync(totals, 0, 16 * 4, st));
-  k_scan_pyramid<<<1, 1024, 0, st>>>(pyramid, levels, prefix, totals);
-  LAUNCH_CHECK("k_scan_pyramid");
-  uint32_t h_tot[16];
-  CUDA_TRY(cudaMemcpyAsync(h_tot, totals, sizeof(h_tot), cudaMemcpyDeviceToHost, st));
+  uint32_t* partials = prefix + PW + 1;
+  const unsigned chunks = unsigned((PW + SCAN_CHUNK - 1) / SCAN_CHUNK);
+  k_scan_partials<<<chunks, SCAN_BLOCK, 0, st>>>(pyramid, PW, partials);
+  LAUNCH_CHECK("k_scan_partials");
+  k_scan_finish<<<chunks, SCAN_BLOCK, 0, st>>>(pyramid, PW, partials, prefix);
+  LAUNCH_CHECK("k_scan_finish");
+  uint32_t h_nodes = 0;
+  CUDA_TRY(cudaMemcpyAsync(&h_nodes, prefix + PW, 4, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
-  int64_t nodes = 0;
-  for (int l = 1; l <= levels; ++l) nodes += h_tot[l];
+  const int64_t nodes = h_nodes;
   if (!has_root && nodes == 0) { *n_out = 0; return OBG_OK; }
   const int64_t total = nodes + 1;
   *n_out = total;
@@ -3262,9 +3516,8 @@ int obg_serialize(const uint32_t* pyramid, int levels, int has_root, uint8_t* ou
     return set_err(OBG_EINVAL, "output capacity %lld < %lld bytes", (long long)out_capacity, (long long)total);
   // root byte: the level-1 child mask
   CUDA_TRY(cudaMemcpyAsync(out, pyramid, 1, cudaMemcpyDeviceToDevice, st));
-  const int64_t PW = pyr_words(levels);
   if (nodes > 0) {
-    k_serialize<<<grid_for(PW, 256, sm_count() * 8), 256, 0, st>>>(pyramid, prefix, levels, out);
+    k_serialize<<<grid_for(PW * 32, 256, sm_count() * 16), 256, 0, st>>>(pyramid, prefix, levels, out);
     LAUNCH_CHECK("k_serialize");
   }
   return OBG_OK;

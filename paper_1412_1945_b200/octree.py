@@ -292,7 +292,11 @@ class Octree:
 
     def _root_flag(self) -> bool:
         if self._has_root is None:
-            self._levels()
+            if self._lv is None and self._pyr is None and self._dev is not None:
+                # device tree: the root exists iff level 1 (word 0) is non-empty -- one word, not the pyramid
+                self._has_root = bool(int(self._dev[0].item()) & 0xFF)
+            else:
+                self._levels()
         return bool(self._has_root)
 
     def _mutate(self) -> None:

@@ -614,3 +614,49 @@ def test_device_entry_points_validate_inputs(cuda):
     truth = cuda.zeros((6, 24, 40), dtype=cuda.uint8)
     st = obg.classify_confusion(model, strided, truth)
     assert st.false_pos == int(want.sum())
+
+
+@pytest.mark.parametrize("levels", range(1, 9))
+def test_counts_histogram_all_levels(cuda, levels):
+    """a13 occupancy counts through the histogram kernel (k_hist: shared
+    memory at L <= 5, global at L >= 6) on flat frames -- a single-colour hot
+    spot, uniform-random frames and a noisy gradient, group sizes 1 and 3,
+    CTA ranges that split trees -- against np.bincount of the oracle codes."""
+    rng = np.random.default_rng(100 + levels)
+    h, w = 40, 64
+    const = np.empty((3, h, w, 3), np.uint8)
+    const[...] = rng.integers(0, 256, size=3, dtype=np.uint8)
+    uni = rng.integers(0, 256, size=(4, h, w, 3), dtype=np.uint8)
+    grad = np.clip(np.arange(w)[None, None, :, None] * 3 + rng.integers(-9, 10, size=(5, h, w, 3)), 0,
+                   255).astype(np.uint8)
+    big = rng.integers(0, 256, size=(2, 720, 1280, 3), dtype=np.uint8)
+    big[1, :, :640] = (7, 200, 90)
+    for frames in (const, uni, grad, big):
+        for gs in (1, 3):
+            if len(frames) < gs:
+                continue
+            dev = cuda.from_numpy(frames).cuda()
+            pyr, cnt = obg.build_presence(dev, levels, group_size=gs, counts=True)
+            ref_pyr = obg.build_presence(dev, levels, group_size=gs)
+            assert cuda.equal(pyr, ref_pyr)
+            cnt = cnt.cpu().numpy().view(np.uint32)
+            for g in range(len(frames) // gs):
+                codes = orc.pack_codes(frames[g * gs:(g + 1) * gs], levels).ravel()
+                want = np.bincount(codes, minlength=8 ** levels)
+                assert np.array_equal(cnt[g, 0], want), (levels, gs, g)
+
+
+@pytest.mark.parametrize("levels,n_codes", [(6, 200000), (7, 0), (7, 1500000), (8, 3000), (8, 2500000)])
+def test_device_serializer_large_trees(cuda, levels, n_codes):
+    """obg_serialize (multi-CTA prefix scan) on large trees -- a full depth-7
+    cube (2.4 M nodes), millions of random depth-8 codes spanning many scan
+    chunks -- against the host sparse serialisation; the device bytes also
+    decode back to the same tree."""
+    rng = np.random.default_rng(levels * 7 + n_codes)
+    host = Octree(levels)
+    host._store_codes(np.arange(8 ** levels) if n_codes == 0 else rng.integers(0, 8 ** levels, size=n_codes))
+    want = host.to_bytes()
+    dev_tree = Octree._from_device(host._device(), levels)
+    got = dev_tree.to_bytes()
+    assert got == want
+    assert Octree.from_bytes(got, levels) == host

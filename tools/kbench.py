@@ -15,7 +15,7 @@ from paper_1412_1945_b200 import scenes  # noqa: E402
 
 
 def frames_for(kind, n, levels):
-    cache = f"/tmp/kbench_{kind}_{n}.npy"      # A/B runs (tools/ab.py) reuse the frames
+    cache = f"/tmp/kbench_{kind}_{n}_{levels}.npy"      # A/B runs (tools/ab.py) reuse the frames
     if os.path.exists(cache):
         return np.load(cache)
     f = _frames_for(kind, n, levels)
@@ -36,6 +36,8 @@ def _frames_for(kind, n, levels):
     if kind == "repeat":
         one = scenes.generate(3, n_train=1, n_test=0).train
         return np.repeat(one, n, axis=0)
+    if kind in ("c4uniform", "c4constant"):       # BASELINE config 4 (3840x2160) scenes
+        return scenes.generate(4, n_train=n, n_test=0, levels=levels, variant=kind[2:]).train
     if kind == "uniform":
         return np.random.default_rng(0).integers(0, 256, size=(n, 1080, 1920, 3), dtype=np.uint8)
     raise SystemExit(kind)
@@ -56,17 +58,20 @@ def timeit(fn, reps=20):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["build", "classify", "model", "sharded", "confusion", "framediff", "runavg"])
+    ap.add_argument("what", choices=["build", "counts", "classify", "model", "sharded", "confusion", "framediff", "runavg"])
     ap.add_argument("--frames", type=int, default=64)
     ap.add_argument("--scene", default="c3")
     ap.add_argument("--levels", type=int, default=6)
+    ap.add_argument("--threshold", type=float, default=0.5)
     a = ap.parse_args()
     f = torch.from_numpy(frames_for(a.scene, a.frames, a.levels)).cuda()
     px = f.shape[0] * f.shape[1] * f.shape[2]
-    cfg = obg.ModelConfig(levels=a.levels, threshold=0.5, training_frames=a.frames)
+    cfg = obg.ModelConfig(levels=a.levels, threshold=a.threshold, training_frames=a.frames)
     digest = ""
     if a.what == "build":
         ms = timeit(lambda: obg.build_presence(f, a.levels))
+    elif a.what == "counts":         # presence + a13 occupancy counts (k_hist pass)
+        ms = timeit(lambda: obg.build_presence(f, a.levels, counts=True))
     elif a.what == "model":
         ms = timeit(lambda: obg.build_background_model_device(f, cfg))
         m = obg.build_background_model_device(f, cfg)
