@@ -22,6 +22,7 @@
 #include <string.h>
 #include <stdarg.h>
 #include <type_traits>
+#include <algorithm>
 
 #include "../../include/obg.h"
 
@@ -350,7 +351,16 @@ __device__ __forceinline__ uint32_t rgb_word_scalar(const uint8_t* p) {
 #ifndef OBG_LOAD_POLICY
 #define OBG_LOAD_POLICY 0
 #endif
-#if OBG_LOAD_POLICY
+#if OBG_LOAD_POLICY == 2
+__device__ __forceinline__ uint64_t frame_policy() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+#define OBG_LDV4(W0, W1, W2, W3, P, OFF)                                                               \
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4+" #OFF "], %5;"                \
+               : "=r"(W0), "=r"(W1), "=r"(W2), "=r"(W3) : "l"(P), "l"(frame_policy()))
+#elif OBG_LOAD_POLICY
 __device__ __forceinline__ uint64_t frame_policy() {
   uint64_t pol;
   asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -838,6 +848,12 @@ __device__ __forceinline__ void flush_segment(uint32_t* s_bits, uint32_t* dst, i
   __syncthreads();                                   // bitset clear before the next segment
 }
 
+#ifndef OBG_ALIGN_TREES
+#define OBG_ALIGN_TREES 1
+#endif
+#ifndef OBG_BUILD_NOLOOKUP
+#define OBG_BUILD_NOLOOKUP 0      // experiment: stream the frames without lookups (load-structure bound)
+#endif
 #ifndef OBG_BUILD_PF
 #define OBG_BUILD_PF 0            // > 0: lane 0 bulk-prefetches the warp's chunk this many iterations ahead into L2
 #endif
@@ -893,13 +909,16 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
       if (OBG_BUILD_PF > 0 && lane == 0 && k + OBG_BUILD_PF < n_full)                          \
         prefetch_l2_bulk(fp + OBG_BUILD_PF * STEP, 48 * 32);                                   \
       if (k + STAGES - 1 < n_lane) load_unit_at(fp + (STAGES - 1) * STEP, NXT);                \
-      if (k < n_full) build_unit<L, SMEM_BITS, COUNTS, true>(CUR, bits, cnt, true);            \
+      if (OBG_BUILD_NOLOOKUP) {                                                                \
+        _Pragma("unroll") for (int q_ = 0; q_ < 12; ++q_) sink ^= CUR[q_];                     \
+      } else if (k < n_full) build_unit<L, SMEM_BITS, COUNTS, true>(CUR, bits, cnt, true);     \
       else build_unit<L, SMEM_BITS, COUNTS, false>(CUR, bits, cnt, k < n_lane);                \
       fp += STEP;                                                                              \
       ++k;                                                                                     \
     }
     constexpr int STAGES = 2;
     uint32_t wa[12], wb[12];
+    uint32_t sink = 0;
     if (0 < n_lane) load_unit_at(fp, wa);
     for (int32_t k = 0; k < n_it;) {
       OBG_BUILD_STEP(wa, wb)
@@ -907,6 +926,7 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
       OBG_BUILD_STEP(wb, wa)
     }
 #undef OBG_BUILD_STEP
+    if (OBG_BUILD_NOLOOKUP && sink == 0x9E3779B9u) ws[0] = sink;     // keep the loads (experiment only)
     if constexpr (SMEM_BITS) flush_segment<L, BUILD_BLOCK>(s_bits, ws + tree * WSW, levels_out, seg_end >= u_end);
     u = seg_end;
   }
@@ -2002,6 +2022,180 @@ k_threshold(const uint32_t* __restrict__ counts, int n_regions, int L, int64_t k
 // ===========================================================================
 // prune / leaf->cube
 // ===========================================================================
+// ---------------------------------------------------------------------------
+// K3 (single-GPU model build, <= MC_MAX_TREES trees): bit-sliced merge and
+// path-order conversion in one launch.  Four lanes per node word; a lane
+// loads its share of the trees' words (up to 16 per round, all in flight)
+// and compresses them with a Harley-Seal carry-save tree (15 full adders =
+// 30 LOP3 per 16 words) into a 5-plane bit-sliced counter -- plane i holds
+// bit i of the 32 per-bit-position tree counts; two shuffle + bit-sliced add
+// steps give the word's counts, a borrow chain against k_min the merged
+// word.  No shared-memory counters, one barrier (the path-order words of a
+// tile are written by the CTA that merged it: CTAs own tiles of 2 R' x 4 G'
+// cube rows, every 32-leaf path-order word lies inside one tile, as in
+// k_merge_fused).  k_merge_fused (SWAR byte counters, 3 barriers per slot,
+// ~12x the instructions) remains for > MC_MAX_TREES trees and for the
+// sharded build's count / threshold modes.
+// ---------------------------------------------------------------------------
+#ifndef OBG_MERGE_CSA
+#define OBG_MERGE_CSA 1
+#endif
+constexpr int MC_BLOCK = 256;                      // 64 node words per CTA
+constexpr int MC_SLOTS = MC_BLOCK / 4;
+constexpr int MC_MAX_TREES = 4 * 32;               // two rounds of 16 per lane
+
+__device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xE8;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ void csa(uint32_t& h, uint32_t& l, uint32_t a, uint32_t b, uint32_t c) {
+  h = maj3(a, b, c);
+  l = a ^ b ^ c;
+}
+// 16 words -> planes o[0..4] (counts 0..16)
+__device__ __forceinline__ void harley_seal16(const uint32_t (&v)[16], uint32_t (&o)[5]) {
+  uint32_t ones = 0, twos = 0, fours = 0, eights = 0, ta, tb, fa, fb, ea, eb;
+  csa(ta, ones, ones, v[0], v[1]);   csa(tb, ones, ones, v[2], v[3]);   csa(fa, twos, twos, ta, tb);
+  csa(ta, ones, ones, v[4], v[5]);   csa(tb, ones, ones, v[6], v[7]);   csa(fb, twos, twos, ta, tb);
+  csa(ea, fours, fours, fa, fb);
+  csa(ta, ones, ones, v[8], v[9]);   csa(tb, ones, ones, v[10], v[11]); csa(fa, twos, twos, ta, tb);
+  csa(ta, ones, ones, v[12], v[13]); csa(tb, ones, ones, v[14], v[15]); csa(fb, twos, twos, ta, tb);
+  csa(eb, fours, fours, fa, fb);
+  uint32_t sixteens;
+  csa(sixteens, eights, eights, ea, eb);
+  o[0] = ones; o[1] = twos; o[2] = fours; o[3] = eights; o[4] = sixteens;
+}
+
+// Merged bits of ws word `w` (of region r) over n_groups trees; valid in lane
+// sub == 0 of the four; every lane of the warp must call it.  Zeroes the
+// words it reads (the workspace is handed back all-zero).
+__device__ __forceinline__ uint32_t merge_word_csa(uint32_t* __restrict__ base, int64_t stride, int n_groups,
+                                                   int64_t k_min, bool active, int sub) {
+  uint32_t q[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const int n_k = active ? (n_groups - sub + 3) / 4 : 0;         // trees sub, sub + 4, ...
+  for (int k0 = 0; k0 < n_k; k0 += 16) {
+    uint32_t v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      v[j] = k0 + j < n_k ? __ldcg(base + int64_t(sub + 4 * (k0 + j)) * stride) : 0u;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (v[j]) base[int64_t(sub + 4 * (k0 + j)) * stride] = 0u;
+    uint32_t o[5];
+    harley_seal16(v, o);
+    uint32_t c = 0;                                                // q += o (bit-sliced)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t oi = i < 5 ? o[i] : 0u;
+      const uint32_t s2 = q[i] ^ oi ^ c;
+      c = maj3(q[i], oi, c);
+      q[i] = s2;
+    }
+  }
+#pragma unroll
+  for (int step = 1; step <= 2; step <<= 1) {                      // + lanes sub ^ 1, then sub ^ 2
+    uint32_t c = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t o = __shfl_xor_sync(0xFFFFFFFFu, q[i], step);
+      const uint32_t s2 = q[i] ^ o ^ c;
+      c = maj3(q[i], o, c);
+      q[i] = s2;
+    }
+  }
+  uint32_t borrow = 0;                                             // count >= k_min <=> no borrow
+#pragma unroll
+  for (int i = 0; i < 8; ++i) borrow = ((k_min >> i) & 1) ? (~q[i] | borrow) : (~q[i] & borrow);
+  if ((k_min >> 8) != 0) borrow = 0xFFFFFFFFu;
+  return ~borrow;
+}
+
+__global__ void __launch_bounds__(MC_BLOCK)
+k_merge_tiles(uint32_t* __restrict__ ws, int n_groups, int n_regions, int L, int64_t k_min,
+              uint32_t* __restrict__ cube, uint32_t* __restrict__ out) {
+  __shared__ uint32_t s_m[MC_SLOTS];
+  const int64_t r = blockIdx.y;
+  const int64_t PW = pyr_words(L), CW = cube_words(L), OW = operand_words(L), WSW = ws_words(L);
+  const int64_t stride = WSW * n_regions;
+  const int tid = threadIdx.x, sub = tid & 3, j = tid >> 2;
+  uint32_t* ws_r = ws + r * WSW;
+  uint32_t* cube_r = cube + r * OW;
+  uint32_t* out_r = out + r * PW;
+  if (blockIdx.x == 0) {
+    // levels 1..min(L, 2): words 0 (level 1), 1..2 (level 2)
+    const int T = L < 2 ? L : 2;
+    const int nw = int(level_offset(T + 1));
+    const int l = j == 0 ? 1 : 2;
+    const bool active = j < nw;
+    const int64_t off = !active ? 0 : (l == L ? int64_t(j - level_offset(l)) : CW + j);
+    uint32_t bits = merge_word_csa(ws_r + off, stride, n_groups, k_min, active, sub);
+    if (active && sub == 0) {
+      if (l == 1) bits &= 0xFFu;
+      s_m[j] = bits;
+      if (l == L) cube_r[j - level_offset(l)] = bits;
+    }
+    __syncthreads();
+    if (tid < nw) {
+      const int lw = tid == 0 ? 1 : 2;
+      const uint32_t m = uint32_t(tid - level_offset(lw));
+      const uint32_t* lv = s_m + level_offset(lw);
+      uint32_t word = 0;
+      const int nb = lw == 1 ? 8 : 32;
+      for (int bb = 0; bb < nb; ++bb) {
+        const uint32_t idx = code_to_cube(m * 32u + uint32_t(bb), lw);
+        word |= ((lv[idx >> 5] >> (idx & 31u)) & 1u) << bb;
+      }
+      out_r[tid] = word;
+    }
+    return;
+  }
+  // tile blocks, level l >= 3: 64 tile-major slots per CTA
+  int64_t b = int64_t(blockIdx.x) - 1;
+  int l = 3;
+  for (; l <= L; ++l) {
+    const int64_t nb = (level_words(l) + MC_SLOTS - 1) / MC_SLOTS;
+    if (b < nb) break;
+    b -= nb;
+  }
+  if (l > L) return;
+  const uint32_t WT = 1u << (l - 2);                               // words (and path words) per tile
+  const uint32_t gq_log = uint32_t(l - 2);
+  const uint32_t LW = uint32_t(level_words(l));
+  const uint32_t slot0 = uint32_t(b) * MC_SLOTS;
+  const int64_t loff = level_offset(l);
+  const uint32_t g = slot0 + uint32_t(j);
+  const bool active = g < LW;
+  uint32_t cw = 0;
+  if (active) cw = mf_tile_word(l, g / WT, g % WT);
+  const int64_t off = (l == L) ? int64_t(cw) : CW + loff + cw;
+  const uint32_t bits = merge_word_csa(ws_r + off, stride, n_groups, k_min, active, sub);
+  if (active && sub == 0) {
+    s_m[j] = bits;
+    if (l == L) cube_r[cw] = bits;
+  }
+  __syncthreads();
+  if (uint32_t(tid) < MC_SLOTS && slot0 + uint32_t(tid) < LW) {
+    // path word: R>>1 = rp, G>>2 = gq, B>>2 = p; bit b0 + 2g0 + 4r0 + 8b1 + 16g1
+    const uint32_t gs = slot0 + uint32_t(tid);
+    const uint32_t t = gs / WT, p = gs % WT;
+    const uint32_t rp = t >> gq_log, gq = t & ((1u << gq_log) - 1u);
+    const uint32_t* tw = s_m + (t * WT - slot0);                    // the tile's words (tile-major)
+    const uint32_t half = WT >> 1;
+    uint32_t word = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t g0 = c & 1, r0 = (c >> 1) & 1, g1 = (c >> 2) & 1;
+      const uint32_t dg = g1 * 2u + g0;
+      const uint32_t bit = (dg << l) + 4u * p;
+      const uint32_t wv = tw[r0 * half + (bit >> 5)];
+      const uint32_t nib = (wv >> (bit & 31u)) & 0xFu;
+      word |= ((nib & 3u) | ((nib & 12u) << 6)) << (g0 * 2 + r0 * 4 + g1 * 16);
+    }
+    out_r[loff + (spread3(rp) | (spread3(p) << 1) | (spread3(gq) << 2))] = word;
+  }
+}
+
 __global__ void k_prune(const uint32_t* __restrict__ pyr, int64_t PW, int64_t PW2, int64_t n_trees,
                         uint32_t* __restrict__ out) {
   const int64_t total = PW2 * n_trees;
@@ -2858,6 +3052,33 @@ int obg_pack_codes(const uint8_t* pixels, int64_t n_pixels, int levels, uint32_t
 #ifndef OBG_BYTE_TABLE
 #define OBG_BYTE_TABLE 1
 #endif
+// Units per CTA of the segment-streaming kernels (K1 flat / byte table /
+// L7 halves / histogram): the CTA streams one contiguous range and flushes
+// its shared table at every tree (frame group) boundary inside it.
+//  * candidate A: the range split evenly over the resident CTAs (at least
+//    4 units per thread, but never more than one tree when trees are
+//    smaller than that -- a tiny-frame CTA would otherwise flush 3-4 times);
+//  * candidate B (n_trees <= resident CTAs): every tree cut into k equal
+//    chunks, so no CTA straddles a boundary (one flush each).
+// Cost model per CTA: its units + ~1800 units of streaming time per flush
+// (a flush is ~2 us; one SM streams ~900 units/us).  C1 (30 x 640x480, L5)
+// takes B (141 CTAs with up to two flushes -> 120 with one); C2 / C3 keep A.
+static int64_t choose_units_per_cta(int64_t total_units, int64_t upt, int64_t n_trees, int64_t max_ctas,
+                                    int threads) {
+  constexpr int64_t FLUSH_UNITS = 1800;
+  int64_t a = (total_units + max_ctas - 1) / max_ctas;
+  const int64_t amin = std::min(int64_t(threads) * 4, upt);
+  if (a < amin) a = amin;
+  const int64_t a_segs = std::min<int64_t>(n_trees, (a + upt - 1) / upt + 1);
+  const int64_t cost_a = a + a_segs * FLUSH_UNITS;
+  if (OBG_ALIGN_TREES && n_trees <= max_ctas) {
+    const int64_t k = max_ctas / n_trees;
+    const int64_t b = (upt + k - 1) / k;
+    if (b >= std::min(int64_t(threads), upt) && b + FLUSH_UNITS < cost_a) return b;
+  }
+  return a;
+}
+
 template <int L>
 static int launch_build_flat(const uint8_t* frames, int64_t units_per_frame, int64_t total_units, int group_size,
                              uint32_t* ws, uint32_t* out_pyr, int64_t n_trees, uint32_t* zero_cube, int64_t zero_words,
@@ -2880,9 +3101,7 @@ static int launch_build_flat(const uint8_t* frames, int64_t units_per_frame, int
   }
   const int64_t max_ctas = int64_t(sm_count()) * blocks_per_sm;
   // at least 4 units per thread per CTA so that tiny inputs use few CTAs
-  int64_t per_cta = (total_units + max_ctas - 1) / max_ctas;
-  const int64_t min_per_cta = int64_t(BUILD_BLOCK) * 4;
-  if (per_cta < min_per_cta) per_cta = min_per_cta;
+  const int64_t per_cta = choose_units_per_cta(total_units, units_per_frame * group_size, total_units / (units_per_frame * group_size), max_ctas, BUILD_BLOCK);
   if (per_cta >= (int64_t(1) << 31) - 2 * BUILD_BLOCK)
     return set_err(OBG_EUNSUPPORTED, "too many pixels per launch (%lld units per CTA)", (long long)per_cta);
   const int grid = int((total_units + per_cta - 1) / per_cta);
@@ -3068,8 +3287,7 @@ static int launch_hist(const uint8_t* frames, int64_t units_per_frame, int64_t t
     attr() = occupancy(k_hist<L, SMEM>, HIST_BLOCK, smem);
   }
   const int64_t max_ctas = int64_t(sm_count()) * attr();
-  int64_t per_cta = (total_units + max_ctas - 1) / max_ctas;
-  if (per_cta < int64_t(HIST_BLOCK) * 4) per_cta = int64_t(HIST_BLOCK) * 4;
+  const int64_t per_cta = choose_units_per_cta(total_units, units_per_frame * group_size, total_units / (units_per_frame * group_size), max_ctas, HIST_BLOCK);
   if (per_cta >= (int64_t(1) << 31) - 2 * HIST_BLOCK)
     return set_err(OBG_EUNSUPPORTED, "too many pixels per launch (%lld units per CTA)", (long long)per_cta);
   const int grid = int((total_units + per_cta - 1) / per_cta);
@@ -3102,9 +3320,7 @@ static int launch_build_l7h(const uint8_t* frames, int64_t units_per_frame, int6
     attr() = 1;
   }
   const int64_t max_ctas = sm_count();                   // one CTA per SM
-  int64_t per_cta = (total_units + max_ctas - 1) / max_ctas;
-  const int64_t min_per_cta = int64_t(L7H_BLOCK) * 4;
-  if (per_cta < min_per_cta) per_cta = min_per_cta;
+  const int64_t per_cta = choose_units_per_cta(total_units, units_per_frame * group_size, total_units / (units_per_frame * group_size), max_ctas, L7H_BLOCK);
   if (per_cta >= (int64_t(1) << 31) - 2 * L7H_BLOCK)
     return set_err(OBG_EUNSUPPORTED, "too many pixels per launch (%lld units per CTA)", (long long)per_cta);
   const int grid = int((total_units + per_cta - 1) / per_cta);
@@ -3253,11 +3469,19 @@ int obg_build_model(const uint8_t* frames, int n_frames, int height, int width, 
   const int n_groups = n_frames / group_size;
   const int64_t words = pyr_words(levels) * n_regions;
   if (n_regions > 65535) return set_err(OBG_EUNSUPPORTED, "too many regions (%lld > 65535)", (long long)n_regions);
-  int64_t blocks = 1;                                   // block 0: levels 1..2
-  for (int l = 3; l <= levels; ++l) blocks += mf_blocks(l);
-  k_merge_fused<0><<<dim3(unsigned(blocks), unsigned(n_regions)), dim3(32, MERGE_GROUPS_C), 0, st>>>(
-      static_cast<uint32_t*>(workspace), n_groups, int(n_regions), levels, k_min, out_cube, out_merged, nullptr);
-  LAUNCH_CHECK("k_merge_fused");
+  if (OBG_MERGE_CSA && n_groups <= MC_MAX_TREES) {
+    int64_t blocks = 1;                                   // block 0: levels 1..2
+    for (int l = 3; l <= levels; ++l) blocks += (level_words(l) + MC_SLOTS - 1) / MC_SLOTS;
+    k_merge_tiles<<<dim3(unsigned(blocks), unsigned(n_regions)), MC_BLOCK, 0, st>>>(
+        static_cast<uint32_t*>(workspace), n_groups, int(n_regions), levels, k_min, out_cube, out_merged);
+    LAUNCH_CHECK("k_merge_tiles");
+  } else {
+    int64_t blocks = 1;                                   // block 0: levels 1..2
+    for (int l = 3; l <= levels; ++l) blocks += mf_blocks(l);
+    k_merge_fused<0><<<dim3(unsigned(blocks), unsigned(n_regions)), dim3(32, MERGE_GROUPS_C), 0, st>>>(
+        static_cast<uint32_t*>(workspace), n_groups, int(n_regions), levels, k_min, out_cube, out_merged, nullptr);
+    LAUNCH_CHECK("k_merge_fused");
+  }
   (void)words;
   return finish_operand(out_cube, n_regions, levels, st);
 }

@@ -27,8 +27,8 @@ def frames_for(kind, n, levels):
 
 
 def _frames_for(kind, n, levels):
-    if kind == "c3":
-        return scenes.generate(3, n_train=n, n_test=0).train
+    if kind in ("c0", "c1", "c2", "c3"):          # BASELINE configs 0..3 scenes
+        return scenes.generate(int(kind[1]), n_train=n, n_test=0).train
     if kind == "const":
         f = np.empty((n, 1080, 1920, 3), np.uint8)
         f[...] = (90, 140, 60)
@@ -43,10 +43,26 @@ def _frames_for(kind, n, levels):
     raise SystemExit(kind)
 
 
+GRAPH = "--graph" in sys.argv
+
+
 def timeit(fn, reps=20):
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
+    if GRAPH:          # device time without the host launch overhead: one captured call, replayed
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            fn()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        fn = g.replay
+        fn()
+        torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(reps):
@@ -63,6 +79,7 @@ def main():
     ap.add_argument("--scene", default="c3")
     ap.add_argument("--levels", type=int, default=6)
     ap.add_argument("--threshold", type=float, default=0.5)
+    ap.add_argument("--graph", action="store_true", help="time CUDA-graph replays (no host launch overhead)")
     a = ap.parse_args()
     f = torch.from_numpy(frames_for(a.scene, a.frames, a.levels)).cuda()
     px = f.shape[0] * f.shape[1] * f.shape[2]
