@@ -505,20 +505,29 @@ def run_ours(args):
                  else "k_build_flat"): 1}
     if L >= 7 or not flat:
         launches["k_levels_cube"] = 1
-    launches["k_merge_fused"] = 1
+    launches["k_merge_tiles" if n_train <= 128 else "k_merge_fused"] = 1      # bit-sliced merge up to 128 trees
     if L == 7:
         launches["k_l7_states"] = 1
     cls_kernel = (f"k_classify_flat<{L}>" if L <= 6 else "k_classify_l7" if L == 7 else "k_classify_flat<8>")
     if not flat:
         cls_kernel = "k_classify_generic"
     launches[cls_kernel] = 1
+    if L == 7 and flat:
+        # two launches, each with its shared-memory size; the path the model
+        # does not take exits at once (obg.cu k_classify_l7<OUT, DIRECT>)
+        launches.pop(cls_kernel)
+        cls_kernel = "k_classify_l7<states|cube>"
+        launches["k_classify_l7<states>"] = 1
+        launches["k_classify_l7<cube>"] = 1
     if world > 1:   # sharded build (distributed.py): counts, all-reduce (NCCL), threshold
-        build_k = {k: v for k, v in launches.items() if k not in ("k_merge_fused", cls_kernel, "k_l7_states")}
-        launches = dict(build_k, **{"k_merge_fused<count>": 1, "k_merge_fused<threshold>": 1, cls_kernel: 1})
+        build_k = {k: v for k, v in launches.items()
+                   if k not in ("k_merge_fused", "k_merge_tiles", "k_l7_states") and not k.startswith("k_classify")}
+        cls_k = {k: v for k, v in launches.items() if k.startswith("k_classify")}
+        launches = dict(build_k, **{"k_merge_fused<count>": 1, "k_merge_fused<threshold>": 1}, **cls_k)
         if L == 7:
             launches["k_l7_states"] = 1
     cls_bytes = n_test * P * 4                 # 3 B read + 1 B mask written per pixel
-    build_bytes = n_train * (P * 3 + obg._lib.cube_words(cfg.levels) * 4)
+    build_bytes = n_train * (P * 3 + 8 ** cfg.levels // 8)     # frames read + one leaf bitset per tree
     cls_gbs = cls_bytes / (cls_avg / 1000) / 1e9
     build_gbs = build_bytes / (build_avg / 1000) / 1e9
 
@@ -545,7 +554,7 @@ def run_ours(args):
         b.record(stream)
         torch.cuda.synchronize()
         b256_ms = a.elapsed_time(b) / args.steps
-        b256_bytes = n_test * (P * 3 + obg._lib.cube_words(cfg.levels) * 4)
+        b256_bytes = n_test * (P * 3 + 8 ** cfg.levels // 8)
         build256 = {"frames": n_test, "ms": round(b256_ms, 4),
                     "mpx_s": round(n_test * P / (b256_ms / 1000) / 1e6, 1),
                     "hbm_frac": round(b256_bytes / (b256_ms / 1000) / 1e9 / peak, 4)}

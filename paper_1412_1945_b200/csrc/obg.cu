@@ -83,8 +83,10 @@ __host__ __device__ static constexpr int64_t cube_words(int L) { return level_wo
 // Classify operand per region: the leaf cube, plus for L = 7 a 2-bit state
 // per L=6 cell (16384 words, see k_classify_l7).
 constexpr int64_t S7_CANON_WORDS = 16384;
+// (+ 32 words: [0] = cells with some but not all leaves, [1] = cells with
+// any leaf -- what k_classify_l7 picks its lookup path by)
 __host__ __device__ static constexpr int64_t operand_words(int L) {
-  return cube_words(L) + (L == 7 ? S7_CANON_WORDS : 0);
+  return cube_words(L) + (L == 7 ? S7_CANON_WORDS + 32 : 0);
 }
 
 // Build workspace per tree: the leaf cube, then levels 1..L-1 in cube order
@@ -2227,17 +2229,35 @@ __global__ void k_leaf_cube(const uint32_t* __restrict__ pyr, int64_t PW, int L,
 // (some / all of its 8 leaves present), canonical order i = R6*256 + G6*4 + B6/16,
 // stored after the cube.  State word = SWAR over the 4 cube words of rows
 // (2R6+{0,1}, 2G6+{0,1}): bit pairs (2b, 2b+1) are the children along B'.
-__global__ void k_l7_states(uint32_t* __restrict__ operand, int64_t n_regions) {
-  const int64_t total = S7_CANON_WORDS * n_regions;
-  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < total; k += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t r = k / S7_CANON_WORDS;
-    const uint32_t i = uint32_t(k - r * S7_CANON_WORDS);
-    uint32_t* op = operand + r * operand_words(7);
+// One CTA (1024 threads) per region; also counts the mixed / occupied cells.
+__global__ void __launch_bounds__(1024) k_l7_states(uint32_t* __restrict__ operand) {
+  __shared__ uint32_t s_red[2][32];
+  uint32_t* op = operand + int64_t(blockIdx.x) * operand_words(7);
+  uint32_t mixed = 0, some = 0;
+  for (uint32_t i = threadIdx.x; i < uint32_t(S7_CANON_WORDS); i += 1024) {
     const uint32_t r6 = i >> 8, g6 = (i >> 2) & 63u, q = i & 3u;
     const uint32_t b = (2u * r6) * 512u + (2u * g6) * 4u + q;
     const uint32_t w00 = op[b], w01 = op[b + 4], w10 = op[b + 512], w11 = op[b + 516];
     const uint32_t a = w00 | w01 | w10 | w11, A = w00 & w01 & w10 & w11;
-    op[cube_words(7) + i] = ((a | (a >> 1)) & 0x55555555u) | (((A & (A >> 1)) & 0x55555555u) << 1);
+    const uint32_t sm = (a | (a >> 1)) & 0x55555555u, al = (A & (A >> 1)) & 0x55555555u;
+    op[cube_words(7) + i] = sm | (al << 1);
+    some += __popc(sm);
+    mixed += __popc(sm & ~al);
+  }
+  mixed = __reduce_add_sync(0xFFFFFFFFu, mixed);
+  some = __reduce_add_sync(0xFFFFFFFFu, some);
+  if ((threadIdx.x & 31) == 0) {
+    s_red[0][threadIdx.x >> 5] = mixed;
+    s_red[1][threadIdx.x >> 5] = some;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    mixed = __reduce_add_sync(0xFFFFFFFFu, s_red[0][threadIdx.x]);
+    some = __reduce_add_sync(0xFFFFFFFFu, s_red[1][threadIdx.x]);
+    if (threadIdx.x == 0) {
+      op[cube_words(7) + S7_CANON_WORDS] = mixed;
+      op[cube_words(7) + S7_CANON_WORDS + 1] = some;
+    }
   }
 }
 
@@ -2426,10 +2446,10 @@ k_classify_flat(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_p
 // (2R6+{0,1}, 2G6+{0,1}): bit pairs (2b, 2b+1) are the children along B'.
 // ---------------------------------------------------------------------------
 #ifndef OBG_S7_BLOCK
-#define OBG_S7_BLOCK 512        // 2 CTAs per SM (66 KB state table each): 1024 threads, -12 % at uniform L7
+#define OBG_S7_BLOCK 1024        // 2 CTAs per SM (66 KB state table each): 1024 threads, -12 % at uniform L7
 #endif
 #ifndef OBG_S7_MINB
-#define OBG_S7_MINB 2
+#define OBG_S7_MINB 1
 #endif
 constexpr int S7_BLOCK = OBG_S7_BLOCK;
 constexpr uint32_t S7_ROWW = 257;                          // 64 G6 x 4 words + pad
@@ -2555,11 +2575,9 @@ __device__ __forceinline__ void classify_unit_l7(const uint32_t (&w)[12], const 
 }
 
 template <int OUT>
-__global__ void __launch_bounds__(S7_BLOCK, OBG_S7_MINB)
-k_classify_l7(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_pixels, const uint32_t* __restrict__ cube,
-              uint8_t* __restrict__ mask, unsigned long long* counts) {
-  ConfAcc acc;
-  extern __shared__ uint32_t s_state[];
+__device__ __forceinline__ void classify_l7_states(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_pixels,
+                                                   const uint32_t* __restrict__ cube, uint8_t* __restrict__ mask,
+                                                   ConfAcc& acc, uint32_t* s_state) {
   for (uint32_t i = threadIdx.x; i < 64u * 256u; i += S7_BLOCK)       // states follow the cube (k_l7_states)
     s_state[(i >> 8) * S7_ROWW + (i & 255u)] = __ldg(cube + cube_words(7) + i);
   __syncthreads();
@@ -2583,6 +2601,127 @@ k_classify_l7(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_pix
       }
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// L = 7 classify, cube in shared memory: 7/8 of the 256 KB leaf cube -- the
+// slabs R' < 112, each 512 words + 1 pad word so R' varies the bank -- fill
+// 225 KB of one 1024-thread CTA's shared memory; pixels with R' >= 112
+// (R >= 224) read the remaining 32 KB from global memory, where it stays
+// L1-resident.  One direct lookup per pixel whatever the model looks like:
+// the state-table kernel (k_classify_l7) needs a random cube gather from
+// L1/L2 for every pixel in a partially filled L6 cell, which a half-full
+// model turns into 0.16 of HBM.
+// ---------------------------------------------------------------------------
+constexpr int C7_BLOCK = 1024;
+#ifndef OBG_L7_PATH
+#define OBG_L7_PATH 0            // 0: by the model's cell counts, 1: state table always, 2: cube always
+#endif
+constexpr uint32_t C7_SLAB = 513;                          // words per R' slab (128 G' x 4) + pad
+constexpr uint32_t C7_ROWS = 112;                          // R' slabs held in shared memory
+constexpr uint32_t C7_WORDS = C7_ROWS * C7_SLAB;           // 57456 words = 229824 bytes
+constexpr uint32_t C7_X_LIMIT = C7_ROWS << 25;             // x = [*, G, B, R]: R' = x >> 25
+
+// pixel x = [*, G, B, R]: the leaf word in shared memory (R' < 112) or in the
+// global cube, rotated so that bit 0 is the pixel's leaf (B' & 31 = x >> 17)
+__device__ __forceinline__ uint32_t c7_inrow(uint32_t x) {             // G' * 16 + (B' >> 5) * 4
+  return ((x >> 5) & 0x7F0u) | ((x >> 20) & 0xCu);
+}
+__device__ __forceinline__ uint32_t c7_smem_word(const char* s_base, uint32_t x) {
+  const uint32_t off = __umulhi(x, 1u << 7) * (C7_SLAB * 4u) + c7_inrow(x);
+  const uint32_t wd = *reinterpret_cast<const uint32_t*>(s_base + off);
+  return __funnelshift_r(wd, wd, x >> 17);
+}
+__device__ __forceinline__ uint32_t c7_global_word(const char* __restrict__ cube, uint32_t x) {
+  const uint32_t wd = __ldg(reinterpret_cast<const uint32_t*>(cube + (((x >> 14) & 0x3F800u) | c7_inrow(x))));
+  return __funnelshift_r(wd, wd, x >> 17);
+}
+
+template <int OUT>
+__device__ __forceinline__ void classify_unit_c7(const uint32_t (&w)[12], const char* s_base,
+                                                 const char* __restrict__ cube, uint8_t* mask, int64_t u,
+                                                 ConfAcc& acc) {
+  uint32_t far = 0;
+  for16([&](auto jc) {
+    constexpr int j = decltype(jc)::value;
+    far |= uint32_t(pixel_word_gbr<j>(w) >= C7_X_LIMIT) << j;
+  });
+  uint32_t bg = 0;
+  if (!__any_sync(__activemask(), far != 0u)) {
+    for16([&](auto jc) {                                 // every pixel of the warp's units in shared memory
+      constexpr int j = decltype(jc)::value;
+      bg |= (c7_smem_word(s_base, pixel_word_gbr<j>(w)) & 1u) << j;
+    });
+  } else {
+    for16([&](auto jc) {                                 // bright-red pixels read the cube's last 16 slabs
+      constexpr int j = decltype(jc)::value;
+      const uint32_t x = pixel_word_gbr<j>(w);
+      const uint32_t v = ((far >> j) & 1u) ? c7_global_word(cube, x) : c7_smem_word(s_base, x);
+      bg |= (v & 1u) << j;
+    });
+  }
+  emit_bits<OUT>(bg, mask, u, acc);
+}
+
+template <int OUT>
+__device__ __forceinline__ void classify_l7_cube(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_pixels,
+                                                 const uint32_t* __restrict__ cube, uint8_t* __restrict__ mask,
+                                                 ConfAcc& acc, uint32_t* s_cube) {
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(cube);
+    for (uint32_t i = threadIdx.x; i < C7_ROWS * 128u; i += C7_BLOCK) {   // 128 uint4 per slab
+      const uint4 v = __ldg(src + i);
+      uint32_t* d = s_cube + (i >> 7) * C7_SLAB + (i & 127u) * 4u;
+      d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+    }
+  }
+  __syncthreads();
+  const char* s_base = reinterpret_cast<const char*>(s_cube);
+  const char* cb = reinterpret_cast<const char*>(cube);
+  const int64_t stride = int64_t(gridDim.x) * C7_BLOCK;
+  for (int64_t u = int64_t(blockIdx.x) * C7_BLOCK + threadIdx.x; u < n_units; u += 2 * stride) {
+    const bool second = u + stride < n_units;
+    uint32_t wa[12], wb[12];
+    load_unit(frames, u, wa);
+    if (second) load_unit(frames, u + stride, wb);
+    classify_unit_c7<OUT>(wa, s_base, cb, mask, u, acc);
+    if (second) classify_unit_c7<OUT>(wb, s_base, cb, mask, u + stride, acc);
+  }
+  if constexpr (OUT == OUT_U8 || OUT == OUT_CONF_U8) {
+    if (blockIdx.x == 0) {
+      for (int64_t i = n_units * 16 + threadIdx.x; i < n_pixels; i += C7_BLOCK) {
+        const uint32_t x = gbr_word_scalar(frames + 3 * i);
+        const uint32_t v = x < C7_X_LIMIT ? c7_smem_word(s_base, x) : c7_global_word(cb, x);
+        emit1<OUT>((v & 1u) ^ 1u, mask, i, acc);
+      }
+    }
+  }
+}
+
+// The model picks the path (counts from k_l7_states, read on the device, so
+// the launches stay graph-capturable): both kernels are launched, each with
+// its own shared-memory size, and the one not chosen exits at once.
+//  * L6 cells almost all full or empty (mixed < 1/32 of the occupied): the
+//    2-bit state table (66 KB, L1 left for the few gathers) answers almost
+//    every pixel (C4 uniform, full model: 0.21 ms vs 0.36 ms, 32 4K frames);
+//  * otherwise the cube in shared memory, one direct lookup per pixel (a
+//    half-full model 0.96 -> 0.36 ms; C3-like scene at L7 0.15 -> 0.125 ms;
+//    a 15 %-mixed model on uniform frames 0.47 -> 0.19 ms).
+__device__ __forceinline__ bool l7_direct(const uint32_t* __restrict__ operand) {
+  const uint32_t mixed = __ldg(operand + cube_words(7) + S7_CANON_WORDS);
+  const uint32_t some = __ldg(operand + cube_words(7) + S7_CANON_WORDS + 1);
+  return OBG_L7_PATH == 2 || (OBG_L7_PATH == 0 && 32u * mixed >= some && mixed > 0);
+}
+static_assert(S7_BLOCK == C7_BLOCK, "one block size for both L7 paths");
+template <int OUT, bool DIRECT>
+__global__ void __launch_bounds__(C7_BLOCK, 1)
+k_classify_l7(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_pixels, const uint32_t* __restrict__ cube,
+              uint8_t* __restrict__ mask, unsigned long long* counts) {
+  if (l7_direct(cube) != DIRECT) return;
+  ConfAcc acc;
+  extern __shared__ __align__(16) uint32_t s_dyn[];
+  if constexpr (DIRECT) classify_l7_cube<OUT>(frames, n_units, n_pixels, cube, mask, acc, s_dyn);
+  else classify_l7_states<OUT>(frames, n_units, n_pixels, cube, mask, acc, s_dyn);
   flush_conf<OUT>(acc, counts);
 }
 
@@ -3514,7 +3653,7 @@ int obg_prune(const uint32_t* pyramids, int n_trees, int levels, int new_levels,
 
 static int finish_operand(uint32_t* operand, int64_t n_regions, int levels, cudaStream_t st) {
   if (levels != 7 || !operand) return OBG_OK;
-  k_l7_states<<<grid_for(S7_CANON_WORDS * n_regions, 256, sm_count() * 8), 256, 0, st>>>(operand, n_regions);
+  k_l7_states<<<unsigned(n_regions), 1024, 0, st>>>(operand);
   LAUNCH_CHECK("k_l7_states");
   return OBG_OK;
 }
@@ -3603,20 +3742,22 @@ static int launch_classify_flat(const uint8_t* frames, int64_t n_pixels, const u
 template <int OUT>
 static int launch_classify_l7(const uint8_t* frames, int64_t n_pixels, const uint32_t* cube, uint8_t* mask,
                               unsigned long long* counts, cudaStream_t st) {
-  const size_t smem = size_t(S7_WORDS) * 4;
-  static DevCache bps_cache;
-  int& bps = bps_cache();
-  if (bps == 0) {
-    CUDA_TRY(cudaFuncSetAttribute(k_classify_l7<OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    bps = occupancy(k_classify_l7<OUT>, S7_BLOCK, smem);
+  const size_t smem_s = size_t(S7_WORDS) * 4, smem_c = size_t(C7_WORDS) * 4;
+  static DevCache attr;
+  if (!attr()) {
+    CUDA_TRY(cudaFuncSetAttribute(k_classify_l7<OUT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_s)));
+    CUDA_TRY(cudaFuncSetAttribute(k_classify_l7<OUT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_c)));
+    attr() = 1;
   }
   const int64_t n_units = n_pixels / 16;
-  int64_t grid = int64_t(sm_count()) * bps;
-  const int64_t need = (n_units + S7_BLOCK - 1) / S7_BLOCK;
+  int64_t grid = sm_count();
+  const int64_t need = (n_units + C7_BLOCK - 1) / C7_BLOCK;
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
-  k_classify_l7<OUT><<<unsigned(grid), S7_BLOCK, smem, st>>>(frames, n_units, n_pixels, cube, mask, counts);
-  LAUNCH_CHECK("k_classify_l7");
+  k_classify_l7<OUT, false><<<unsigned(grid), C7_BLOCK, smem_s, st>>>(frames, n_units, n_pixels, cube, mask, counts);
+  LAUNCH_CHECK("k_classify_l7<states>");
+  k_classify_l7<OUT, true><<<unsigned(grid), C7_BLOCK, smem_c, st>>>(frames, n_units, n_pixels, cube, mask, counts);
+  LAUNCH_CHECK("k_classify_l7<cube>");
   return OBG_OK;
 }
 
