@@ -551,6 +551,15 @@ __device__ __forceinline__ void pair_positions_dyn(const uint32_t (&w)[12], int 
   }
 }
 
+// compile-time loop over the 16 pixels of a unit: f(std::integral_constant<int, J>)
+template <int J = 0, class F>
+__device__ __forceinline__ void for16(F&& f) {
+  if constexpr (J < 16) {
+    f(std::integral_constant<int, J>{});
+    for16<J + 1>(f);
+  }
+}
+
 template <int J, int L>
 __device__ __forceinline__ void unpack16(const uint32_t (&w)[12], uint32_t (&px)[16]) {
   px[J] = pixel_operand<L, J>(w);
@@ -1383,6 +1392,155 @@ k_build_l7h(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t
       __syncthreads();
       u = seg_end;
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// L = 7 build, ONE pass: 7/8 of the tree's 256 KB leaf set -- 112 of the 128
+// R' slabs (512 words each, word index XOR-swizzled by the slab's low bits so
+// R' varies the bank) -- in shared memory (224 KB; fewer slabs, leaving L1
+// to the frame loads, measured slower: 96 / 80 / 64 slabs +13 / +40 / +63 %
+// on uniform frames); the other 16 slabs, a
+// window chosen per CTA opposite the R' of its range's first pixel (so a
+// single-colour scene never lands there), straight in the tree's workspace
+// cube in global memory (checked through L1, set with atomics: a stale L1
+// copy only costs a redundant atomic).  Shared slab s holds R' = (s + 16 +
+// g0) & 127.  Word offsets of a pixel pair ride in the two 16-bit halves of
+// one register (slab << 9 | swizzled in-slab word < 65536) as in K1.
+// k_build_l7h instead streams its range once per cube half (two frame reads).
+// 1024 threads, one CTA per SM, dynamic smem at the fixed 1 KB window.
+// ---------------------------------------------------------------------------
+constexpr int L7C_BLOCK = 1024;
+#ifndef OBG_L7B_SLABS
+#define OBG_L7B_SLABS 112        // R' slabs (of 128) in shared memory; the rest is left to L1 for the frame loads
+#endif
+constexpr uint32_t L7C_N = OBG_L7B_SLABS;
+constexpr uint32_t L7C_W = 128u - L7C_N;                 // global window
+constexpr uint32_t L7C_WORDS = L7C_N * 512u;
+
+// pixels 2K, 2K+1: byte addresses in shared memory (valid where !far),
+// rotate amounts of the leaf bit, far flags (bit 0) and packed R' / in-row
+// words for the global path.  k7 = ((L7C_N - g0) & 127) * 0x00010001.
+template <int K>
+__device__ __forceinline__ void l7c_pair(const uint32_t (&w)[12], uint32_t k7, uint32_t& addr_a, uint32_t& addr_b,
+                                         uint32_t& bsel_a, uint32_t& bsel_b, uint32_t& far_a, uint32_t& far_b,
+                                         uint32_t& rq, uint32_t& q) {
+  constexpr int o = 6 * K, a = o >> 2, b = o & 3;
+  constexpr uint32_t selR = uint32_t(b) | (uint32_t(b) << 4) | (uint32_t(b + 3) << 8) | (uint32_t(b + 3) << 12);
+  constexpr uint32_t selG = uint32_t(b + 1) | (uint32_t(b + 2) << 4) | (uint32_t(b + 4) << 8) | (uint32_t(b + 5) << 12);
+  const uint32_t yR = __byte_perm(w[a], w[a + 1], selR);                 // [R_A, R_A, R_B, R_B]
+  const uint32_t yG = __byte_perm(w[a], w[a + 1], selG);                 // [G_A, B_A, G_B, B_B]
+  rq = __umulhi(yR, 1u << 31) & 0x007F007Fu;                             // R' per half
+  const uint32_t P = (rq + k7) & 0x007F007Fu;                            // shared slab (+ 112 .. 127: far)
+  const uint32_t bq = __umulhi(yG, 1u << 18) & 0x00030003u;              // B >> 6 per half
+  q = (yG & 0x00FE00FEu) * 2u + bq;                                      // G' * 4 + B' >> 5 per half
+  const uint32_t pair = (P << 9) | (q ^ (P & 0x001F001Fu));              // swizzled word offsets
+  addr_a = (pair << 2) & 0x3FFFCu;
+  addr_b = __umulhi(pair, 1u << 18) & ~3u;
+  bsel_a = __umulhi(yG, 1u << 23);
+  bsel_b = __umulhi(yG, 1u << 7);
+  far_a = (P & 0x7Fu) >= L7C_N;
+  far_b = (P >> 16) >= L7C_N;
+}
+
+template <int K>
+__device__ __forceinline__ void build_pairs_l7c(const uint32_t (&w)[12], bool valid, uint32_t k7,
+                                                uint32_t* __restrict__ gcube) {
+  uint32_t ad[4], bs[4], fr[4], v[4], go[4];
+  {
+    uint32_t rq0, q0, rq1, q1;
+    l7c_pair<K>(w, k7, ad[0], ad[1], bs[0], bs[1], fr[0], fr[1], rq0, q0);
+    l7c_pair<K + 1>(w, k7, ad[2], ad[3], bs[2], bs[3], fr[2], fr[3], rq1, q1);
+    go[0] = ((rq0 & 0x7Fu) << 11) | ((q0 & 0xFFFFu) << 2);              // canonical cube byte offsets
+    go[1] = ((rq0 >> 16) << 11) | ((q0 >> 16) << 2);
+    go[2] = ((rq1 & 0x7Fu) << 11) | ((q1 & 0xFFFFu) << 2);
+    go[3] = ((rq1 >> 16) << 11) | ((q1 >> 16) << 2);
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint32_t wd;
+    if (!fr[j]) wd = lds_at(ad[j]);
+    else wd = __ldca(reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(gcube) + go[j]));
+    v[j] = __funnelshift_r(wd, wd, bs[j]);
+  }
+  const bool miss = valid && !(v[0] & v[1] & v[2] & v[3] & 1u);
+  if (__any_sync(0xFFFFFFFFu, miss)) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (valid && !(v[j] & 1u)) {
+        const uint32_t bit = 1u << (bs[j] & 31u);
+        if (!fr[j]) reds_or_at(ad[j], bit);
+        else atomicOr(reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(gcube) + go[j]), bit);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void build_unit_l7c(const uint32_t (&w)[12], bool valid, uint32_t k7,
+                                               uint32_t* __restrict__ gcube) {
+  build_pairs_l7c<0>(w, valid, k7, gcube);
+  build_pairs_l7c<2>(w, valid, k7, gcube);
+  build_pairs_l7c<4>(w, valid, k7, gcube);
+  build_pairs_l7c<6>(w, valid, k7, gcube);
+}
+
+__global__ void __launch_bounds__(L7C_BLOCK, 1)
+k_build_l7c(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t total_units, int group_size,
+            int64_t units_per_cta, uint32_t* __restrict__ ws, uint32_t* __restrict__ out_pyr, int64_t n_trees,
+            uint32_t* __restrict__ zero_cube, int64_t zero_words) {
+  extern __shared__ __align__(1024) uint32_t s_bits[];
+  if (static_cast<uint32_t>(__cvta_generic_to_shared(s_bits)) != DYN_SMEM_BASE) __trap();
+  constexpr int64_t WSW = ws_words(7);
+  if (blockIdx.x == 0) {
+    clear_shared_words(out_pyr, n_trees, 7);
+    for (int64_t i = threadIdx.x; i < zero_words; i += L7C_BLOCK) zero_cube[i] = 0u;
+  }
+  const int64_t u_begin = int64_t(blockIdx.x) * units_per_cta;
+  const int64_t u_end = min(total_units, u_begin + units_per_cta);
+  if (u_begin >= u_end) return;
+  for (uint32_t i = threadIdx.x; i < L7C_WORDS; i += L7C_BLOCK) s_bits[i] = 0u;
+  __syncthreads();
+  // the global window: L7C_W R' slabs opposite the R' of the range's first pixel
+  const uint32_t g0 = ((uint32_t(__ldg(frames + 48 * u_begin)) >> 1) + 64u - L7C_W / 2u) & 127u;
+  const uint32_t k7 = ((L7C_N - g0) & 127u) * 0x00010001u;
+  const int64_t upt = units_per_frame * group_size;
+  const int lane = threadIdx.x & 31;
+  int64_t u = u_begin;
+  while (u < u_end) {
+    const int64_t tree = u / upt;
+    const int64_t seg_end = min(u_end, (tree + 1) * upt);
+    uint32_t* dst = ws + tree * WSW;
+    const int64_t seg_len = seg_end - u;
+    const int32_t rel0 = int32_t(threadIdx.x) - lane;
+    const int32_t n_it = seg_len > rel0 ? int32_t((seg_len - rel0 + L7C_BLOCK - 1) / L7C_BLOCK) : 0;
+    const int32_t n_lane = seg_len > rel0 + lane ? int32_t((seg_len - rel0 - lane + L7C_BLOCK - 1) / L7C_BLOCK) : 0;
+    constexpr int64_t STEP = 48 * int64_t(L7C_BLOCK);
+    const uint8_t* fp = frames + 48 * (u + rel0 + lane);
+    uint32_t wa[12], wb[12];
+    if (0 < n_lane) load_unit_at(fp, wa);
+    for (int32_t k = 0; k < n_it;) {
+      if (k + 1 < n_lane) load_unit_at(fp + STEP, wb);
+      build_unit_l7c(wa, k < n_lane, k7, dst);
+      fp += STEP;
+      if (++k >= n_it) break;
+      if (k + 1 < n_lane) load_unit_at(fp + STEP, wa);
+      build_unit_l7c(wb, k < n_lane, k7, dst);
+      fp += STEP;
+      ++k;
+    }
+    // flush the shared slabs into the tree's leaf cube, leave them zeroed
+    __syncthreads();
+    for (uint32_t p = threadIdx.x; p < L7C_WORDS; p += L7C_BLOCK) {
+      const uint32_t x = s_bits[p];
+      if (x) {
+        const uint32_t sl = p >> 9, c = (p & 511u) ^ (sl & 31u);
+        const uint32_t r = (sl + L7C_W + g0) & 127u;              // the slab's R'
+        atomicOr(dst + ((r << 9) | c), x);
+        s_bits[p] = 0u;
+      }
+    }
+    __syncthreads();
+    u = seg_end;
   }
 }
 
@@ -2494,15 +2652,6 @@ __device__ __forceinline__ uint32_t l7_leaf_word_if(const char* __restrict__ cub
                : "+r"(wd) : "l"(cube + off), "r"(pred));
   return __funnelshift_r(wd, wd, x >> 17);
 }
-// compile-time loop over the 16 pixels of a unit: f(std::integral_constant<int, J>)
-template <int J = 0, class F>
-__device__ __forceinline__ void for16(F&& f) {
-  if constexpr (J < 16) {
-    f(std::integral_constant<int, J>{});
-    for16<J + 1>(f);
-  }
-}
-
 // 16 background bits (bit j = pixel j's leaf present) -> the unit's output
 template <int OUT>
 __device__ __forceinline__ void emit_bits(uint32_t bg, uint8_t* out, int64_t u, ConfAcc& acc) {
@@ -3449,9 +3598,30 @@ static int launch_hist_any(int L, const uint8_t* frames, int64_t upf, int64_t to
   }
 }
 
+#ifndef OBG_L7_ONEPASS
+#define OBG_L7_ONEPASS 1
+#endif
 static int launch_build_l7h(const uint8_t* frames, int64_t units_per_frame, int64_t total_units, int group_size,
                             uint32_t* ws, uint32_t* out_pyr, int64_t n_trees, uint32_t* zero_cube, int64_t zero_words,
                             cudaStream_t st) {
+  if (OBG_L7_ONEPASS) {
+    constexpr size_t smem = size_t(L7C_WORDS) * 4;
+    static DevCache attr;
+    if (!attr()) {
+      CUDA_TRY(cudaFuncSetAttribute(k_build_l7c, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      attr() = 1;
+    }
+    const int64_t max_ctas = sm_count();
+    const int64_t per_cta = choose_units_per_cta(total_units, units_per_frame * group_size,
+                                                 total_units / (units_per_frame * group_size), max_ctas, L7C_BLOCK);
+    if (per_cta >= (int64_t(1) << 31) - 2 * L7C_BLOCK)
+      return set_err(OBG_EUNSUPPORTED, "too many pixels per launch (%lld units per CTA)", (long long)per_cta);
+    const int grid = int((total_units + per_cta - 1) / per_cta);
+    k_build_l7c<<<grid, L7C_BLOCK, smem, st>>>(frames, units_per_frame, total_units, group_size, per_cta, ws, out_pyr,
+                                               n_trees, zero_cube, zero_words);
+    LAUNCH_CHECK("k_build_l7c");
+    return OBG_OK;
+  }
   constexpr size_t smem = size_t(L7H_ALLOC) * 4;
   static DevCache attr;
   if (!attr()) {
