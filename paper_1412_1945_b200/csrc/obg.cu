@@ -1456,12 +1456,22 @@ __device__ __forceinline__ void build_pairs_l7c(const uint32_t (&w)[12], bool va
     go[2] = ((rq1 & 0x7Fu) << 11) | ((q1 & 0xFFFFu) << 2);
     go[3] = ((rq1 >> 16) << 11) | ((q1 >> 16) << 2);
   }
+  if (!__any_sync(0xFFFFFFFFu, (fr[0] | fr[1] | fr[2] | fr[3]) != 0u)) {
+    // no pixel of the warp's 4-pixel group in the global window (the common
+    // case away from the window, e.g. a single-colour scene): shared only
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    uint32_t wd;
-    if (!fr[j]) wd = lds_at(ad[j]);
-    else wd = __ldca(reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(gcube) + go[j]));
-    v[j] = __funnelshift_r(wd, wd, bs[j]);
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t wd = lds_at(ad[j]);
+      v[j] = __funnelshift_r(wd, wd, bs[j]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint32_t wd;
+      if (!fr[j]) wd = lds_at(ad[j]);
+      else wd = __ldca(reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(gcube) + go[j]));
+      v[j] = __funnelshift_r(wd, wd, bs[j]);
+    }
   }
   const bool miss = valid && !(v[0] & v[1] & v[2] & v[3] & 1u);
   if (__any_sync(0xFFFFFFFFu, miss)) {
