@@ -1075,7 +1075,9 @@ static int launch_build_band(const uint8_t* frames, int n_frames_used, int H, in
     attr_smem() = int(smem);
   }
   const int64_t band_units = (int64_t(H) / R + 1) * (W / 16);
-  const int64_t per_band = (int64_t(sm_count()) + R - 1) / R;   // one CTA per SM in total
+  // one CTA per SM in total, R bands x per_band within ONE wave (rounding
+  // up put 3 x 50 CTAs on 148 SMs: a second wave of two CTAs for the 3x4 grid)
+  const int64_t per_band = std::max<int64_t>(1, int64_t(sm_count()) / R);
   int64_t per_cta = (band_units * n_frames_used + per_band - 1) / per_band;
   const int64_t min_per_cta = int64_t(BUILD_BLOCK) * 4;
   if (per_cta < min_per_cta) per_cta = min_per_cta;
@@ -2961,18 +2963,27 @@ k_classify_band(const uint8_t* __restrict__ frames, int n_frames, int H, int W, 
   const int64_t upf = int64_t(H) * W16;                         // units per frame
   const int band_units = (y1 - y0) * W16;
   const char* sb = reinterpret_cast<const char*>(s_ops);
-  for (int f = 0; f < n_frames; ++f) {
-    const int64_t ubase = int64_t(f) * upf + int64_t(y0) * W16;
-    const int stride = int(gridDim.x) * BAND_BLOCK;
-    for (int k0 = int(blockIdx.x) * BAND_BLOCK + int(threadIdx.x); k0 < band_units; k0 += 2 * stride) {
-      // two units per iteration: six 16-byte loads in flight
-      uint32_t wa[12], wb[12];
-      const bool second = k0 + stride < band_units;
-      load_unit(frames, ubase + k0, wa);
-      if (second) load_unit(frames, ubase + k0 + stride, wb);
-      band_unit<L, OUT>(wa, k0, ubase, W16, C, s_cb, sb, mask, acc);
-      if (second) band_unit<L, OUT>(wb, k0 + stride, ubase, W16, C, s_cb, sb, mask, acc);
+  // the band's units of ALL frames as one index space, so the grid is sized
+  // by the work (every SM busy) rather than by one frame's band
+  const int64_t total = int64_t(band_units) * n_frames;
+  const int64_t stride = int64_t(gridDim.x) * BAND_BLOCK;
+  for (int64_t k = int64_t(blockIdx.x) * BAND_BLOCK + threadIdx.x; k < total; k += 2 * stride) {
+    // two units per iteration: six 16-byte loads in flight
+    uint32_t wa[12], wb[12];
+    const int fa = int(k / band_units), ka = int(k - int64_t(fa) * band_units);
+    const int64_t ubase_a = int64_t(fa) * upf + int64_t(y0) * W16;
+    const bool second = k + stride < total;
+    int kb = 0;
+    int64_t ubase_b = 0;
+    load_unit(frames, ubase_a + ka, wa);
+    if (second) {
+      const int fb = int((k + stride) / band_units);
+      kb = int(k + stride - int64_t(fb) * band_units);
+      ubase_b = int64_t(fb) * upf + int64_t(y0) * W16;
+      load_unit(frames, ubase_b + kb, wb);
     }
+    band_unit<L, OUT>(wa, ka, ubase_a, W16, C, s_cb, sb, mask, acc);
+    if (second) band_unit<L, OUT>(wb, kb, ubase_b, W16, C, s_cb, sb, mask, acc);
   }
   flush_conf<OUT>(acc, counts);
 }
@@ -2987,9 +2998,11 @@ static int launch_classify_band(const uint8_t* frames, int n_frames, int H, int 
     attr_smem() = int(smem);
   }
   const int bps = occupancy(k_classify_band<L, OUT>, BAND_BLOCK, smem);
-  const int64_t per_band = (int64_t(sm_count()) * bps + R - 1) / R;
+  // R bands x per_band CTAs within one wave (rounding up would leave a
+  // second wave of a few CTAs: 3 x 50 on 148 SMs doubled the 3x4 time)
+  const int64_t per_band = std::max<int64_t>(1, int64_t(sm_count()) * bps / R);
   const int64_t band_units = (int64_t(H) / R + 1) * (W / 16);
-  int64_t gx = min(per_band, (band_units + BAND_BLOCK - 1) / BAND_BLOCK);
+  int64_t gx = min(per_band, (band_units * n_frames + BAND_BLOCK - 1) / BAND_BLOCK);
   if (gx < 1) gx = 1;
   k_classify_band<L, OUT><<<dim3(unsigned(gx), unsigned(R)), BAND_BLOCK, smem, st>>>(frames, n_frames, H, W, R, C, cube,
                                                                                     mask, counts);
