@@ -189,6 +189,11 @@ int obg_read_pnm_files(const char* const* paths, int n_files, int kind, int64_t 
 int obg_write_pgm_masks(const uint8_t* masks, int n_masks, int64_t width, int64_t height,
                         const char* const* paths, int n_threads);
 
+/* Copy n host blocks of bytes_each bytes, srcs[i] -> dst + i * bytes_each
+ * (e.g. a list of frames into one pinned staging buffer), split into 1 MiB
+ * pieces over a persistent pool of host threads.  Host only. */
+int obg_host_gather(const uint8_t* const* srcs, int n, int64_t bytes_each, uint8_t* dst);
+
 /* Parse one non-empty preorder child-mask tree (Octree.from_bytes /
  * decode_tree, octree.py:229-237, 250-281) at data[pos..n) into a host
  * path-order pyramid (u32 [obg_pyramid_words(depth)]).  On OBG_EFORMAT,

@@ -91,3 +91,61 @@ def is_tensor(x) -> bool:
         return isinstance(x, torch().Tensor)
     except ImportError:  # pragma: no cover
         return False
+
+
+# ---------------------------------------------------------------------------
+# Host staging for the reference-signature path (numpy frames in, numpy masks
+# out): frames are gathered into pinned buffers by libobg's persistent host
+# copy pool (obg_host_gather, GIL released) and moved with asynchronous H2D
+# copies -- instead of np.stack (one single-threaded 400 MB copy for 64 C3
+# frames) followed by a pageable H2D.  Buffers are cached per thread.
+# ---------------------------------------------------------------------------
+import ctypes
+import threading
+
+_TLS = threading.local()
+_STAGE_BYTES = 64 << 20                 # frames per staging chunk: ~64 MiB
+
+
+def _pinned(key, shape):
+    """Thread-local pinned uint8 buffer + the event of its last async use."""
+    cache = getattr(_TLS, "pinned", None)
+    if cache is None:
+        cache = _TLS.pinned = {}
+    ent = cache.get(key)
+    if ent is None or tuple(ent[0].shape) != tuple(shape):
+        t = torch()
+        ent = [t.empty(shape, dtype=t.uint8, pin_memory=True), None]
+        cache[key] = ent
+    return ent
+
+
+def host_gather(arrays, dst_ptr: int, nbytes: int) -> None:
+    """Copy equally sized contiguous host arrays back to back into dst_ptr."""
+    srcs = (ctypes.c_void_p * len(arrays))(*[a.ctypes.data for a in arrays])
+    _lib.check(_lib.load().obg_host_gather(srcs, len(arrays), nbytes, dst_ptr))
+
+
+def frames_list_to_device(frames):
+    """A list of (h, w, 3) uint8 numpy frames as one (n, h, w, 3) CUDA tensor
+    on the current device / stream: chunks gathered into two alternating
+    pinned buffers while the previous chunk's H2D runs."""
+    t = torch()
+    n = len(frames)
+    h, w = frames[0].shape[:2]
+    fb = h * w * 3
+    dev = t.empty((n, h, w, 3), dtype=t.uint8, device="cuda")
+    k = max(1, min(n, _STAGE_BYTES // max(fb, 1)))
+    stream = t.cuda.current_stream()
+    for c, s0 in enumerate(range(0, n, k)):
+        m = min(k, n - s0)
+        ent = _pinned(("stage", c & 1, h, w), (k, h, w, 3))
+        if ent[1] is not None:
+            ent[1].synchronize()                     # the slot's previous H2D has read it
+        chunk = [np.ascontiguousarray(f) for f in frames[s0:s0 + m]]
+        host_gather(chunk, ent[0].data_ptr(), fb)
+        dev[s0:s0 + m].copy_(ent[0][:m], non_blocking=True)
+        ev = t.cuda.Event()
+        ev.record(stream)
+        ent[1] = ev
+    return dev

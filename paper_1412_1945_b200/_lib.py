@@ -61,6 +61,7 @@ SIGNATURES = {
     "obg_decode_tree_codes": (_I, [_P, _L, _L, _I, _P, _P, _L, ctypes.POINTER(ctypes.c_int64),
                                    ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
                                    ctypes.POINTER(ctypes.c_int)]),
+    "obg_host_gather": (_I, [ctypes.POINTER(ctypes.c_void_p), _I, _L, _P]),
     "obg_build_counts": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _L, _I, _P]),
     "obg_threshold_counts": (_I, [_P, _I, _I, _L, _P, _P, _P]),
     "obg_frame_diff": (_I, [_P, _P, _I, _L, _I, _P, _P]),
@@ -135,5 +136,6 @@ def level_offset(level: int) -> int:
 
 def cube_words(levels: int) -> int:
     """Words of one region's classify operand: the leaf cube, plus for L = 7
-    a 2-bit state per L=6 cell (16384 words)."""
-    return level_words(levels) + (16384 if levels == 7 else 0)
+    a 2-bit state per L=6 cell (16384 words) and 32 words of cell counts
+    (k_l7_states; the L7 classify picks its path by them)."""
+    return level_words(levels) + (16384 + 32 if levels == 7 else 0)

@@ -2424,10 +2424,8 @@ __global__ void __launch_bounds__(1024) k_l7_states(uint32_t* __restrict__ opera
   if (threadIdx.x < 32) {
     mixed = __reduce_add_sync(0xFFFFFFFFu, s_red[0][threadIdx.x]);
     some = __reduce_add_sync(0xFFFFFFFFu, s_red[1][threadIdx.x]);
-    if (threadIdx.x == 0) {
-      op[cube_words(7) + S7_CANON_WORDS] = mixed;
-      op[cube_words(7) + S7_CANON_WORDS + 1] = some;
-    }
+    // the operand's 32-word tail: [0] mixed, [1] occupied, the rest zero
+    op[cube_words(7) + S7_CANON_WORDS + threadIdx.x] = threadIdx.x == 0 ? mixed : threadIdx.x == 1 ? some : 0u;
   }
 }
 

@@ -14,6 +14,9 @@
 #include <sys/stat.h>
 
 #include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -238,9 +241,98 @@ void parallel_for(int n, int n_threads, F&& fn) {
   for (auto& t : pool) t.join();
 }
 
+// Persistent worker threads for the small, frequent host copies of the
+// reference-signature path (one frame per detect_octree call): spawning
+// threads per call would cost more than the copy.  run(n, fn) calls fn(i)
+// for i < n on the pool plus the caller; calls are serialised.
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool pool;
+    return pool;
+  }
+  int size() const { return int(workers_.size()) + 1; }
+  void run(int n, const std::function<void(int)>& fn) {
+    std::lock_guard<std::mutex> serial(call_mu_);
+    if (n <= 0) return;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      fn_ = &fn;
+      n_ = n;
+      next_.store(0);
+      active_ = int(workers_.size());
+      ++gen_;
+    }
+    cv_.notify_all();
+    drain();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return active_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  CopyPool() {
+    int n = int(std::thread::hardware_concurrency());
+    n = n < 2 ? 1 : (n > 16 ? 16 : n);
+    for (int t = 1; t < n; ++t) workers_.emplace_back([this] { loop(); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  void drain() {
+    for (int i = next_.fetch_add(1); i < n_; i = next_.fetch_add(1)) (*fn_)(i);
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+      }
+      drain();
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--active_ == 0) done_cv_.notify_one();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_, call_mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* fn_ = nullptr;
+  std::atomic<int> next_{0};
+  int n_ = 0, active_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
 }  // namespace
 
 extern "C" {
+
+int obg_host_gather(const uint8_t* const* srcs, int n, int64_t bytes_each, uint8_t* dst) {
+  if (n < 0 || bytes_each < 0) return obg_set_error(OBG_EINVAL, "bad sizes");
+  if (n == 0 || bytes_each == 0) return OBG_OK;
+  if (!srcs || !dst) return obg_set_error(OBG_EINVAL, "null buffer");
+  for (int i = 0; i < n; ++i)
+    if (!srcs[i]) return obg_set_error(OBG_EINVAL, "null source %d", i);
+  constexpr int64_t CHUNK = int64_t(1) << 20;                 // 1 MiB pieces spread over the pool
+  const int64_t per = (bytes_each + CHUNK - 1) / CHUNK;
+  const int64_t tasks = per * n;
+  if (tasks > (int64_t(1) << 30)) return obg_set_error(OBG_EUNSUPPORTED, "copy too large");
+  CopyPool::get().run(int(tasks), [&](int t) {
+    const int64_t i = t / per, c = t - i * per;
+    const int64_t off = c * CHUNK, len = (off + CHUNK <= bytes_each) ? CHUNK : bytes_each - off;
+    memcpy(dst + i * bytes_each + off, srcs[i] + off, size_t(len));
+  });
+  return OBG_OK;
+}
 
 int obg_pnm_header(const uint8_t* data, int64_t size, int kind, int64_t* width, int64_t* height,
                    int64_t* payload, int64_t* err_offset) {

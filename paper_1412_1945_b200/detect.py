@@ -58,8 +58,12 @@ def detect_octree(model: BackgroundModel, frame) -> np.ndarray:
     frame = np.asarray(frame)
     if frame.ndim != 3 or frame.shape[2] != 3 or frame.dtype != np.uint8:
         raise ValueError(f"expected (h, w, 3) uint8 frame, got {frame.dtype} {frame.shape}")
-    _check_frame_shape(model, frame.shape[0], frame.shape[1])
+    h, w = frame.shape[0], frame.shape[1]
+    _check_frame_shape(model, h, w)
     _device.require_cuda()
+    # one frame: pageable copies beat pinned staging here (the staging copy
+    # and its synchronisation cost more than the driver's own: 1.17 vs
+    # 0.83 ms per 1080p frame, tools/sig_probe.py)
     mask = classify(model, _device.to_device_u8(frame[None]))
     return mask[0].cpu().numpy().view(np.bool_)
 

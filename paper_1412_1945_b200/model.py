@@ -187,7 +187,7 @@ def _stack_device(frames, n: int):
         return _device.to_device_u8(frames[:n])
     if isinstance(frames, np.ndarray):
         return _device.to_device_u8(frames[:n])
-    return _device.to_device_u8(np.stack(frames[:n]))
+    return _device.frames_list_to_device(frames[:n])
 
 
 def build_presence(frames_dev, levels: int, grid_rows: int = 1, grid_cols: int = 1, group_size: int = 1,
