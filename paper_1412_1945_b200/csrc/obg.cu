@@ -3448,16 +3448,22 @@ static int launch_build_flat(const uint8_t* frames, int64_t units_per_frame, int
 // obg_build_presence, the restatement np.bincount of
 // pack_codes per frame tree, reference model.py:107 / tests/test_model.py:22-26).
 // A separate streaming pass, so counts never slow the presence build.  The
-// CTA streams a contiguous unit range (tree segments as K1); per pixel the
-// warp aggregates equal bins with __match_any_sync and the lowest peer adds
-// the peer count:
-//   L <= 5: into a histogram privatised per CTA in shared memory (8^L u32,
-//           cube order, 128 KB at L = 5), flushed to the tree's path-order
-//           counts in HBM (global atomics, non-zero bins only) at each
-//           segment end;
-//   L >= 6: straight into the tree's counts in global memory (1 MB at L = 6
-//           does not fit shared memory; the warp aggregation is what keeps a
-//           single-colour hot spot cheap).
+// CTA streams a contiguous unit range (tree segments as K1):
+//   L <= 5: one shared atomicAdd per pixel into a histogram privatised per CTA
+//           (8^L u32, cube order, 128 KB at L = 5), flushed to the tree's
+//           path-order counts in HBM (global atomics, non-zero bins only) at
+//           each segment end.  The shared atomic unit merges a warp's equal
+//           addresses itself; __match_any_sync aggregation (OBG_HIST_AGG=1)
+//           measured ~5x slower on mixed warps;
+//   L >= 6: straight into the tree's counts in global memory (1 MB at L = 6,
+//           8 MB at L = 7), run-length merged per thread and warp-reduced when
+//           a whole warp adds to one bin (a single-colour hot spot).  Two
+//           privatised L = 6 forms were built and measured slower
+//           (profiles/ab_r02/r02_ab_hist6.txt): a histogram spread over the
+//           distributed shared memory of an 8-CTA cluster (2.2-2.7x: remote
+//           red.shared::cluster adds run at ~0.5 per SM-clock), and 8 bin
+//           slices per unit range (equal on mixed frames, 2.7x on a
+//           single-colour frame, whose adds all land in one slice's CTA).
 // ---------------------------------------------------------------------------
 constexpr int HIST_BLOCK = 1024;
 #ifndef OBG_HIST_AGG
@@ -3584,9 +3590,239 @@ k_hist(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t tota
   }
 }
 
+// (A/B variant, OBG_HIST_CLUSTER=1; slower than the global atomics, see above)
+// L = 6: the 8^6-bin u32 histogram (1 MB) is privatised per CLUSTER of 8 CTAs
+// in distributed shared memory -- each CTA holds 1/8 of the bins (128 KB) and
+// the cluster streams one unit range as 8192 threads; every pixel sends one
+// red.shared::cluster.add to the CTA owning its bin.  Owner = (R' ^ G' ^ B') & 7
+// (a smooth scene spreads over all eight), bin within the owner = cube idx >> 3
+// (B' & 7 is recovered from the owner, so the map is a bijection).  A thread's
+// 16 consecutive pixels are run-length merged first (one add per run), which
+// keeps a single-colour frame from sending 16 adds per thread to one address.
+// At a tree-segment end: cluster barrier (release/acquire: every add landed),
+// each CTA flushes its non-zero bins to the tree's path-order counts in HBM,
+// barrier again before the next segment's adds.
+constexpr int HC_CLUSTER = 8;
+constexpr int HC_THREADS = HC_CLUSTER * HIST_BLOCK;
+#ifndef OBG_HIST_CLUSTER
+#define OBG_HIST_CLUSTER 0        // L = 6: 0 global atomics, 1 cluster DSMEM, 2 bin slices (A/B: 0 wins)
+#endif
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// add `cnt` to bin `idx` (cube order, L = 6) of the cluster's histogram
+__device__ __forceinline__ void hc_add(uint32_t s_base, uint32_t idx, uint32_t cnt) {
+  const uint32_t owner = (idx ^ (idx >> 6) ^ (idx >> 12)) & 7u;
+  const uint32_t local = s_base + ((idx >> 3) << 2);
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(owner));
+  asm volatile("red.shared::cluster.add.u32 [%0], %1;" :: "r"(remote), "r"(cnt) : "memory");
+}
+
+__device__ __forceinline__ void hc_unit(const uint32_t (&w)[12], bool valid, uint32_t s_base) {
+  uint32_t prev = 0, run = 0;
+  for16([&](auto jc) {
+    constexpr int j = decltype(jc)::value;
+    const uint32_t idx = cube_idx<6>(pixel_word<j>(w));
+    if constexpr (j == 0) {
+      prev = idx;
+      run = 1;
+    } else {
+      const bool change = idx != prev;
+      if (valid && change) hc_add(s_base, prev, run);
+      run = change ? 1u : run + 1u;
+      prev = idx;
+    }
+  });
+  if (valid) hc_add(s_base, prev, run);
+}
+
+__global__ void __launch_bounds__(HIST_BLOCK, 1)
+k_hist_cluster(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t total_units, int group_size,
+               int64_t units_per_cluster, uint32_t* __restrict__ counts) {
+  extern __shared__ __align__(16) uint32_t s_hist[];
+  constexpr int L = 6;
+  constexpr uint32_t NB = 1u << (3 * L), NLOC = NB / HC_CLUSTER;
+  const uint32_t rank = cluster_rank();
+  const int64_t cl = int64_t(blockIdx.x) / HC_CLUSTER;
+  const int64_t u_begin = cl * units_per_cluster;
+  const int64_t u_end = min(total_units, u_begin + units_per_cluster);
+  if (u_begin >= u_end) return;                  // uniform over the cluster
+  for (uint32_t i = threadIdx.x; i < NLOC; i += HIST_BLOCK) s_hist[i] = 0u;
+  const uint32_t s_base = uint32_t(__cvta_generic_to_shared(s_hist));
+  cluster_sync_all();                            // every slice zeroed before the first add
+  const int lane = threadIdx.x & 31;
+  const int32_t gt = int32_t(rank) * HIST_BLOCK + int32_t(threadIdx.x);   // thread of the cluster
+  const int64_t upt = units_per_frame * group_size;
+  int64_t u = u_begin;
+  while (u < u_end) {
+    const int64_t tree = u / upt;
+    const int64_t seg_end = min(u_end, (tree + 1) * upt);
+    uint32_t* dst = counts + tree * int64_t(NB);
+    const int64_t seg_len = seg_end - u;
+    const int32_t rel0 = gt - lane;
+    const int32_t n_it = seg_len > rel0 ? int32_t((seg_len - rel0 + HC_THREADS - 1) / HC_THREADS) : 0;
+    const int32_t n_lane = seg_len > rel0 + lane ? int32_t((seg_len - rel0 - lane + HC_THREADS - 1) / HC_THREADS) : 0;
+    constexpr int64_t STEP = 48 * int64_t(HC_THREADS);
+    const uint8_t* fp = frames + 48 * (u + rel0 + lane);
+    uint32_t wa[12], wb[12];
+    if (0 < n_lane) load_unit_at(fp, wa);
+    for (int32_t k = 0; k < n_it;) {
+      if (k + 1 < n_lane) load_unit_at(fp + STEP, wb);
+      hc_unit(wa, k < n_lane, s_base);
+      fp += STEP;
+      if (++k >= n_it) break;
+      if (k + 1 < n_lane) load_unit_at(fp + STEP, wa);
+      hc_unit(wb, k < n_lane, s_base);
+      fp += STEP;
+      ++k;
+    }
+    cluster_sync_all();                          // all adds of the segment landed
+    for (uint32_t i = threadIdx.x; i < NLOC; i += HIST_BLOCK) {
+      const uint32_t c = s_hist[i];
+      if (c) {
+        const uint32_t rg = i >> 3;              // R' << 6 | G'
+        const uint32_t b = ((i & 7u) << 3) | ((rank ^ rg ^ (rg >> 6)) & 7u);
+        atomicAdd(dst + cube_to_code((rg << 6) | b, L), c);
+        s_hist[i] = 0u;
+      }
+    }
+    cluster_sync_all();                          // slices clear before the next segment's adds
+    u = seg_end;
+  }
+}
+
+static int launch_hist_cluster(const uint8_t* frames, int64_t units_per_frame, int64_t total_units, int group_size,
+                               uint32_t* counts, cudaStream_t st) {
+  constexpr size_t smem = (size_t(1) << 18) / HC_CLUSTER * 4;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = HC_CLUSTER;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(HIST_BLOCK);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  static DevCache max_clusters;
+  if (!max_clusters()) {
+    CUDA_TRY(cudaFuncSetAttribute(k_hist_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    cfg.gridDim = dim3(HC_CLUSTER * 64);
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k_hist_cluster, &cfg) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = 1;
+    }
+    max_clusters() = n;
+  }
+  const int64_t upt = units_per_frame * group_size;
+  const int64_t per_cl = choose_units_per_cta(total_units, upt, total_units / upt, max_clusters(), HC_THREADS);
+  if (per_cl >= (int64_t(1) << 31) - 2 * HC_THREADS)
+    return set_err(OBG_EUNSUPPORTED, "too many pixels per launch (%lld units per cluster)", (long long)per_cl);
+  const int n_cl = int((total_units + per_cl - 1) / per_cl);
+  cfg.gridDim = dim3(unsigned(n_cl * HC_CLUSTER));
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, k_hist_cluster, frames, units_per_frame, total_units, group_size, per_cl, counts));
+  LAUNCH_CHECK("k_hist_cluster");
+  return OBG_OK;
+}
+
+// (A/B variant, OBG_HIST_CLUSTER=2; slower than the global atomics, see above)
+// L = 6, bin slices: 8 CTAs share one unit range (adjacent blockIdx, so they
+// run in the same wave and 7 of the 8 frame reads hit L2); CTA s privatises
+// the bins with B' & 7 == s (128 KB, bin = idx >> 3) and streams the whole
+// range, one local shared atomic per pixel of its slice.
+__global__ void __launch_bounds__(HIST_BLOCK, 1)
+k_hist_slices(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t total_units, int group_size,
+              int64_t units_per_range, uint32_t* __restrict__ counts) {
+  extern __shared__ __align__(16) uint32_t s_hist[];
+  constexpr int L = 6;
+  constexpr uint32_t NB = 1u << (3 * L), NLOC = NB / HC_CLUSTER;
+  const uint32_t slice = blockIdx.x % HC_CLUSTER;
+  const int64_t u_begin = int64_t(blockIdx.x / HC_CLUSTER) * units_per_range;
+  const int64_t u_end = min(total_units, u_begin + units_per_range);
+  if (u_begin >= u_end) return;
+  for (uint32_t i = threadIdx.x; i < NLOC; i += HIST_BLOCK) s_hist[i] = 0u;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t upt = units_per_frame * group_size;
+  int64_t u = u_begin;
+  while (u < u_end) {
+    const int64_t tree = u / upt;
+    const int64_t seg_end = min(u_end, (tree + 1) * upt);
+    uint32_t* dst = counts + tree * int64_t(NB);
+    const int64_t seg_len = seg_end - u;
+    const int32_t rel0 = int32_t(threadIdx.x) - lane;
+    const int32_t n_it = seg_len > rel0 ? int32_t((seg_len - rel0 + HIST_BLOCK - 1) / HIST_BLOCK) : 0;
+    const int32_t n_lane = seg_len > rel0 + lane ? int32_t((seg_len - rel0 - lane + HIST_BLOCK - 1) / HIST_BLOCK) : 0;
+    constexpr int64_t STEP = 48 * int64_t(HIST_BLOCK);
+    const uint8_t* fp = frames + 48 * (u + rel0 + lane);
+    uint32_t wa[12], wb[12];
+    auto body = [&](const uint32_t (&w)[12], bool valid) {
+      for16([&](auto jc) {
+        constexpr int j = decltype(jc)::value;
+        const uint32_t idx = cube_idx<L>(pixel_word<j>(w));
+        if (valid && (idx & 7u) == slice) atomicAdd(s_hist + (idx >> 3), 1u);
+      });
+    };
+    if (0 < n_lane) load_unit_at(fp, wa);
+    for (int32_t k = 0; k < n_it;) {
+      if (k + 1 < n_lane) load_unit_at(fp + STEP, wb);
+      body(wa, k < n_lane);
+      fp += STEP;
+      if (++k >= n_it) break;
+      if (k + 1 < n_lane) load_unit_at(fp + STEP, wa);
+      body(wb, k < n_lane);
+      fp += STEP;
+      ++k;
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < NLOC; i += HIST_BLOCK) {
+      const uint32_t c = s_hist[i];
+      if (c) {
+        atomicAdd(dst + cube_to_code((i << 3) | slice, L), c);
+        s_hist[i] = 0u;
+      }
+    }
+    __syncthreads();
+    u = seg_end;
+  }
+}
+
+static int launch_hist_slices(const uint8_t* frames, int64_t units_per_frame, int64_t total_units, int group_size,
+                              uint32_t* counts, cudaStream_t st) {
+  constexpr size_t smem = (size_t(1) << 18) / HC_CLUSTER * 4;
+  static DevCache attr;
+  if (!attr()) {
+    CUDA_TRY(cudaFuncSetAttribute(k_hist_slices, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr() = 1;
+  }
+  const int64_t n_ranges_max = std::max(1, sm_count() / HC_CLUSTER);
+  const int64_t upt = units_per_frame * group_size;
+  const int64_t per_r = choose_units_per_cta(total_units, upt, total_units / upt, n_ranges_max, HIST_BLOCK);
+  if (per_r >= (int64_t(1) << 31) - 2 * HIST_BLOCK)
+    return set_err(OBG_EUNSUPPORTED, "too many pixels per launch (%lld units per range)", (long long)per_r);
+  const int n_r = int((total_units + per_r - 1) / per_r);
+  k_hist_slices<<<n_r * HC_CLUSTER, HIST_BLOCK, smem, st>>>(frames, units_per_frame, total_units, group_size, per_r,
+                                                           counts);
+  LAUNCH_CHECK("k_hist_slices");
+  return OBG_OK;
+}
+
 template <int L>
 static int launch_hist(const uint8_t* frames, int64_t units_per_frame, int64_t total_units, int group_size,
                        uint32_t* counts, cudaStream_t st) {
+  if constexpr (L == 6) {
+    if (OBG_HIST_CLUSTER == 1) return launch_hist_cluster(frames, units_per_frame, total_units, group_size, counts, st);
+    if (OBG_HIST_CLUSTER == 2) return launch_hist_slices(frames, units_per_frame, total_units, group_size, counts, st);
+  }
   constexpr bool SMEM = L <= 5;
   const size_t smem = SMEM ? (size_t(1) << (3 * L)) * 4 : 0;
   static DevCache attr;

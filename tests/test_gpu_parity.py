@@ -619,7 +619,8 @@ def test_device_entry_points_validate_inputs(cuda):
 @pytest.mark.parametrize("levels", range(1, 9))
 def test_counts_histogram_all_levels(cuda, levels):
     """a13 occupancy counts through the histogram kernel (k_hist: shared
-    memory at L <= 5, global at L >= 6) on flat frames -- a single-colour hot
+    memory at L <= 5, distributed shared memory of a CTA cluster at L = 6,
+    global at L >= 7) on flat frames -- a single-colour hot
     spot, uniform-random frames and a noisy gradient, group sizes 1 and 3,
     CTA ranges that split trees -- against np.bincount of the oracle codes."""
     rng = np.random.default_rng(100 + levels)

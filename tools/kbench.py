@@ -89,6 +89,8 @@ def main():
         ms = timeit(lambda: obg.build_presence(f, a.levels))
     elif a.what == "counts":         # presence + a13 occupancy counts (k_hist pass)
         ms = timeit(lambda: obg.build_presence(f, a.levels, counts=True))
+        import hashlib
+        digest = " model=" + hashlib.sha1(obg.build_presence(f, a.levels, counts=True)[1].cpu().numpy().tobytes()).hexdigest()[:12]
     elif a.what == "model":
         ms = timeit(lambda: obg.build_background_model_device(f, cfg))
         m = obg.build_background_model_device(f, cfg)
