@@ -26,6 +26,7 @@ OBG_EIO = -5
 WS_ZEROED = 1
 MASK_U8 = 0
 MASK_PACKED = 1
+MASK_AFTER_MODEL = 0x100    # OBG_MASK_AFTER_MODEL: classify launched as a dependent of the model build
 
 # Every symbol declared in include/obg.h, with its ctypes signature.
 _P = ctypes.c_void_p

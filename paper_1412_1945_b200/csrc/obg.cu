@@ -66,6 +66,62 @@ extern "C" int obg_set_error(int code, const char* fmt, ...) {
   } while (0)
 
 // ---------------------------------------------------------------------------
+// Programmatic dependent launch (PDL).  A model build is K1 -> merge and the
+// bench step K1 -> merge -> classify, each kernel a few to a few hundred us:
+// the launch gap and ramp of the next kernel (~2 us each) is 5-25 % of the
+// small configurations.  The secondary kernel is launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization: its CTAs are placed as
+// the primary's drain and park at griddepcontrol.wait, which returns once the
+// primary grid has completed and its writes are visible.  Primaries call
+// griddepcontrol.launch_dependents at their start (they are one resident wave,
+// so the dependents only take SMs that are already free).  Both instructions
+// are no-ops in a launch without the attribute.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Primaries trigger their dependents early only when their grid leaves most
+// SMs free (C0: 20 CTAs, model build 12.6 -> 10.6 us); a full-width K1 is
+// slower with dependents parked behind it (C3 +1.5 us), so it lets the
+// implicit trigger at completion stand (C3 -0.7 us, C2 -0.4 us against plain
+// stream order).  profiles/ab_r02/r02_ab_pdl.txt
+#ifndef OBG_PDL_EARLY_GRID
+#define OBG_PDL_EARLY_GRID 64
+#endif
+constexpr unsigned PDL_EARLY_GRID = OBG_PDL_EARLY_GRID;
+// OBG_PDL (environment): 0 no dependent launches, 1 (default) the merge, 2 also a
+// classify flagged OBG_MASK_AFTER_MODEL.  Measured on whole bench steps (3 runs,
+// profiles/ab_r02/r02_ab_pdl_step.txt): level 1 -0.1 .. -0.5 us on every config;
+// level 2 a further -1.3 us at C2 (146 us step) but +2.4 us at C3 (592 classify
+// CTAs parked behind the merge), so the flag is honoured only at level 2.
+static int pdl_level() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("OBG_PDL");
+    v = (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 1;
+  }
+  return v;
+}
+
+// kernel<<<grid, block, smem, st>>>(args...), as a programmatic dependent of
+// the previous kernel in the stream when `pdl`
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_dep(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int pdl,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (pdl > 0 && pdl_level() >= pdl) ? 1 : 0;          // pdl: 0 never, 1 / 2 = the level that enables it
+  return cudaLaunchKernelEx(&cfg, kernel, KArgs(args)...);
+}
+
+// ---------------------------------------------------------------------------
 // layout helpers (host + device)
 // ---------------------------------------------------------------------------
 __host__ __device__ static constexpr int64_t level_words(int l) {
@@ -880,6 +936,7 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
   if constexpr (SMEM_BITS) {
     if (static_cast<uint32_t>(__cvta_generic_to_shared(s_bits)) != DYN_SMEM_BASE) __trap();
   }
+  if (gridDim.x <= PDL_EARLY_GRID) pdl_launch_dependents();   // SMs are free: the merge's CTAs may take them now
   constexpr int64_t CW = cube_words(L), WSW = ws_words(L);
   if (blockIdx.x == 0) {
     clear_shared_words(out_pyr, n_trees, L);
@@ -1193,6 +1250,7 @@ k_build_bytes(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64
   using T = ByteTab<L>;
   extern __shared__ __align__(1024) uint32_t s_tab[];
   if (static_cast<uint32_t>(__cvta_generic_to_shared(s_tab)) != DYN_SMEM_BASE) __trap();
+  if (gridDim.x <= PDL_EARLY_GRID) pdl_launch_dependents();   // SMs are free: the merge's CTAs may take them now
   uint32_t* s_bits = s_tab + T::BITS_OFF / 4;
   constexpr int64_t WSW = ws_words(L);
   if (blockIdx.x == 0) {
@@ -1238,6 +1296,234 @@ k_build_bytes(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64
     pack_byte_table<L>(s_tab, s_bits, !last);
     flush_segment<L, BUILD_BLOCK>(s_bits, ws + tree * WSW, levels_out, last);
     u = seg_end;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1 through a TMA ring (L <= 6).  Same segment streaming, lookups and flush
+// as k_build_flat / k_build_bytes, but the frame bytes reach the SM by bulk
+// async copies: one cp.async.bulk per CTA iteration (its 1024 units = 48 KB,
+// contiguous in the frame batch) into a ring of RING_STAGES stages, each with
+// an mbarrier; lanes read their 48-byte unit back with three conflict-free
+// LDS.128.  Why (ncu r02 of k_build_flat<6>: L1/TEX 71 % busy, long-scoreboard
+// the top stall, 60 % issue active):
+//  * the register-pipelined kernel keeps one unit per thread in flight (49 KB
+//    per SM, about what 6.4 TB/s x ~1.2 us needs with nothing to spare), the
+//    ring RING_STAGES x 48 KB without a register;
+//  * a 48-byte-strided LDG.128 touches 12 lines per warp instruction and the
+//    three loads of a unit touch the same 12: 36 L1 tag wavefronts per 1536
+//    bytes against 12 for the ring's LDS, and none for the bulk copy;
+//  * the copies keep streaming across tree boundaries while the CTA flushes
+//    its bitset, so the segment clear / flush / drain (~5 us at C3) overlaps.
+// No producer warp: the warp that releases a stage LAST (a shared counter per
+// stage) issues that stage's refill, RING_STAGES iterations ahead, so nobody
+// waits for a slot.  tools/probes/ring_probe.cu: this ring streams 6.7 TB/s
+// (the LDG pattern 6.4); a private 1.5 KB ring per warp only 2.6-3.6 TB/s
+// (many small bulk copies in flight), which is why the ring is per CTA.
+// ---------------------------------------------------------------------------
+#ifndef OBG_RING_STAGES
+#define OBG_RING_STAGES 3
+#endif
+#ifndef OBG_RING_RELAXED
+#define OBG_RING_RELAXED 1        // stage release without a CTA fence (see ring_release)
+#endif
+#ifndef OBG_BUILD_RING
+#define OBG_BUILD_RING 0          // 1: K1 through the TMA ring (A/B: slower, see above)
+#endif
+constexpr int RING_STAGES = OBG_RING_STAGES;
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "OBG_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@p bra OBG_DONE;\n\t"
+      "bra OBG_WAIT;\n\t"
+      "OBG_DONE:\n\t}"
+      :: "r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void lds_unit(uint32_t addr, uint32_t (&w)[12]) {
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "r"(addr));
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4+16];" : "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]) : "r"(addr));
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4+32];" : "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]) : "r"(addr));
+}
+// release of a ring stage by one warp: returns how many warps released it before
+__device__ __forceinline__ uint32_t ring_release(uint32_t cnt_addr) {
+  uint32_t old;
+#if OBG_RING_RELAXED
+  asm volatile("atom.relaxed.cta.shared.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(cnt_addr) : "memory");
+#else
+  asm volatile("atom.acq_rel.cta.shared.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(cnt_addr) : "memory");
+#endif
+  return old;
+}
+
+// Shared-memory plan of k_build_ring: the table(s) of the lookup kernels at
+// the dynamic base, then the ring stages, the mbarriers and the release counters.
+template <int L, bool BYTES, int NT>
+struct RingPlan {
+  static constexpr uint32_t table_bytes() {
+    if constexpr (BYTES) return ByteTab<L>::BITS_OFF + uint32_t(Smem<L>::alloc_words) * 4u;
+    else return uint32_t(Smem<L>::alloc_words) * 4u;
+  }
+  static constexpr uint32_t STAGE = uint32_t(NT) * 48u;                 // one CTA iteration
+  static constexpr uint32_t RING_OFF = (table_bytes() + 127u) & ~127u;
+  static constexpr uint32_t BAR_OFF = RING_OFF + RING_STAGES * STAGE;
+  static constexpr uint32_t CNT_OFF = BAR_OFF + RING_STAGES * 8u;
+  static constexpr uint32_t CUR_OFF = (CNT_OFF + RING_STAGES * 4u + 15u) & ~15u;   // RingCursor per stage
+  static constexpr uint32_t TOTAL = CUR_OFF + RING_STAGES * 24u;
+  static_assert(TOTAL <= 227u * 1024u, "ring does not fit shared memory");
+};
+
+// The producer's position: the next CTA iteration (segment [u, end), k-th
+// block of BUILD_BLOCK units) a stage will be refilled with.  One cursor per
+// stage in shared memory, each stepping RING_STAGES iterations at a time, and
+// touched only by the thread that refills that stage (refills of one stage are
+// ordered by its mbarrier / release counter), so the streaming warps carry no
+// producer state.
+struct RingCursor {
+  int64_t u, end;      // current segment (tree piece) of the CTA's range; u >= u_end: no more work
+  int32_t k;           // iteration within the segment
+  int32_t pad;
+};
+__device__ __forceinline__ void ring_advance(RingCursor& c, int64_t u_end, int64_t upt, int block) {
+  if (c.u >= u_end) return;
+  const int32_t n = int32_t((c.end - c.u + block - 1) / block);
+  if (++c.k >= n) {
+    c.u = c.end;
+    c.end = min(u_end, c.u + upt);
+    c.k = 0;
+  }
+}
+
+template <int L, bool BYTES>
+__global__ void __launch_bounds__(BUILD_BLOCK, 1)
+k_build_ring(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t total_units,
+             int group_size, int64_t units_per_cta, uint32_t* __restrict__ ws,
+             uint32_t* __restrict__ out_pyr, int64_t n_trees, uint32_t* __restrict__ zero_cube,
+             int64_t zero_words, int levels_out) {
+  using P = RingPlan<L, BYTES, BUILD_BLOCK>;
+  constexpr uint32_t NW = BUILD_BLOCK / 32;
+  extern __shared__ __align__(1024) uint32_t s_dyn[];
+  if (static_cast<uint32_t>(__cvta_generic_to_shared(s_dyn)) != DYN_SMEM_BASE) __trap();
+  if (gridDim.x <= PDL_EARLY_GRID) pdl_launch_dependents();   // SMs are free: the merge's CTAs may take them now
+  uint32_t* s_bits = s_dyn;
+  if constexpr (BYTES) s_bits = s_dyn + ByteTab<L>::BITS_OFF / 4;
+  constexpr int64_t WSW = ws_words(L);
+  const int lane = threadIdx.x & 31;
+  const int32_t rel0 = int32_t(threadIdx.x) - lane;                    // warp's first unit of an iteration
+  const int64_t u_begin = int64_t(blockIdx.x) * units_per_cta;
+  const int64_t u_end = min(total_units, u_begin + units_per_cta);
+  const int64_t upt = units_per_frame * group_size;                    // units per tree
+  constexpr uint32_t ring0 = DYN_SMEM_BASE + P::RING_OFF;
+  constexpr uint32_t bar0 = DYN_SMEM_BASE + P::BAR_OFF;
+  constexpr uint32_t cnt0 = DYN_SMEM_BASE + P::CNT_OFF;
+  RingCursor* s_cur = reinterpret_cast<RingCursor*>(reinterpret_cast<char*>(s_dyn) + P::CUR_OFF);
+
+  // refill stage `slot` with its cursor's iteration and step the cursor (one thread)
+  auto refill = [&](uint32_t slot) {
+    RingCursor c = s_cur[slot];
+    if (c.u >= u_end) return;
+    const int64_t first = c.u + int64_t(c.k) * BUILD_BLOCK;
+    const uint32_t bytes = uint32_t(min(int64_t(BUILD_BLOCK), c.end - first)) * 48u;
+    mbar_expect_tx(bar0 + slot * 8u, bytes);
+    bulk_g2s(ring0 + slot * P::STAGE, frames + 48 * first, bytes, bar0 + slot * 8u);
+#pragma unroll
+    for (int s = 0; s < RING_STAGES; ++s) ring_advance(c, u_end, upt, BUILD_BLOCK);
+    s_cur[slot] = c;
+  };
+
+  if (u_begin < u_end && threadIdx.x == 0) {
+    RingCursor c;
+    c.u = u_begin;
+    c.end = min(u_end, (u_begin / upt + 1) * upt);
+    c.k = 0;
+    c.pad = 0;
+#pragma unroll
+    for (int s = 0; s < RING_STAGES; ++s) {
+      mbar_init(bar0 + s * 8u, 1u);
+      s_dyn[P::CNT_OFF / 4 + s] = 0u;
+      s_cur[s] = c;
+      ring_advance(c, u_end, upt, BUILD_BLOCK);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#pragma unroll
+    for (int s = 0; s < RING_STAGES; ++s) refill(uint32_t(s));         // in flight during the clears below
+  }
+  if (blockIdx.x == 0) {
+    clear_shared_words(out_pyr, n_trees, L);
+    for (int64_t i = threadIdx.x; i < zero_words; i += BUILD_BLOCK) zero_cube[i] = 0u;
+  }
+  if (u_begin >= u_end) return;
+  if constexpr (BYTES) {
+    for (uint32_t i = threadIdx.x; i < ByteTab<L>::BYTES / 16; i += BUILD_BLOCK)
+      reinterpret_cast<uint4*>(s_dyn)[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  for (uint32_t i = threadIdx.x; i < Smem<L>::compact; i += BUILD_BLOCK) s_bits[Smem<L>::compact_word(i)] = 0u;
+  __syncthreads();                                                     // tables clear, barriers initialised
+
+  uint32_t c_slot = 0, c_phase = 0;
+  const uint32_t unit_off = ring0 + uint32_t(threadIdx.x) * 48u;
+  // take this warp's unit of the next CTA iteration out of the ring, release
+  // the stage and (last warp out) refill it
+  auto fetch = [&](uint32_t (&w)[12], bool any) {
+    mbar_wait(bar0 + c_slot * 8u, c_phase);
+    if (any) lds_unit(unit_off + c_slot * P::STAGE, w);
+    __syncwarp();                                                      // every lane holds its unit
+    if (lane == 0 && ring_release(cnt0 + c_slot * 4u) == NW - 1u) {
+      s_dyn[P::CNT_OFF / 4 + c_slot] = 0u;
+      refill(c_slot);
+    }
+    if (++c_slot == RING_STAGES) { c_slot = 0; c_phase ^= 1u; }
+  };
+  int64_t u = u_begin;
+  int64_t seg_end = min(u_end, (u_begin / upt + 1) * upt);
+  while (u < u_end) {
+    const int64_t tree = u / upt;
+    const int32_t seg_len = int32_t(seg_end - u);                      // < 2^31 (host checks units_per_cta)
+    const int32_t n_it = (seg_len + BUILD_BLOCK - 1) / BUILD_BLOCK;
+    int32_t left = seg_len - rel0;                                     // units from this warp's first to the segment end
+    // the next unit comes out of the ring while the current one is looked up
+    // (two register buffers swapped by unrolling, as in k_build_flat)
+#define OBG_RING_STEP(CUR, NXT)                                                               \
+    {                                                                                          \
+      if (k + 1 < n_it) fetch(NXT, left > BUILD_BLOCK);                                        \
+      if (left >= 32) {                                                                        \
+        if constexpr (BYTES) build_unit_bytes<L, true>(CUR, true);                             \
+        else build_unit<L, true, false, true>(CUR, s_bits, nullptr, true);                     \
+      } else if (left > 0) {                                                                   \
+        if constexpr (BYTES) build_unit_bytes<L, false>(CUR, lane < left);                     \
+        else build_unit<L, true, false, false>(CUR, s_bits, nullptr, lane < left);             \
+      }                                                                                        \
+      left -= BUILD_BLOCK;                                                                     \
+      ++k;                                                                                     \
+    }
+    uint32_t wa[12], wb[12];
+    fetch(wa, left > 0);
+    for (int32_t k = 0; k < n_it;) {
+      OBG_RING_STEP(wa, wb)
+      if (k >= n_it) break;
+      OBG_RING_STEP(wb, wa)
+    }
+#undef OBG_RING_STEP
+    const bool last = seg_end >= u_end;
+    if constexpr (BYTES) {
+      __syncthreads();                                                 // the segment's table is complete
+      pack_byte_table<L>(s_dyn, s_bits, !last);
+    }
+    flush_segment<L, BUILD_BLOCK>(s_bits, ws + tree * WSW, levels_out, last);
+    u = seg_end;
+    seg_end = min(u_end, u + upt);
   }
 }
 
@@ -2291,6 +2577,8 @@ k_merge_tiles(uint32_t* __restrict__ ws, int n_groups, int n_regions, int L, int
   const int64_t PW = pyr_words(L), CW = cube_words(L), OW = operand_words(L), WSW = ws_words(L);
   const int64_t stride = WSW * n_regions;
   const int tid = threadIdx.x, sub = tid & 3, j = tid >> 2;
+  pdl_wait();                                        // the build kernel's workspace is complete
+  pdl_launch_dependents();                           // a dependent classify may place its CTAs
   uint32_t* ws_r = ws + r * WSW;
   uint32_t* cube_r = cube + r * OW;
   uint32_t* out_r = out + r * PW;
@@ -2568,6 +2856,7 @@ k_classify_flat(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_p
   extern __shared__ uint32_t s_bits[];
   constexpr int64_t CW = cube_words(L);
   const uint32_t* bits = cube;
+  pdl_wait();                                        // OBG_MASK_AFTER_MODEL: the merge's operand is complete
   if constexpr (SMEM_BITS) {
     for (uint32_t i = threadIdx.x; i < SmemC<L>::compact; i += CLS_BLOCK) {
       const uint32_t p = SmemC<L>::compact_word(i);
@@ -3414,6 +3703,24 @@ static int launch_build_flat(const uint8_t* frames, int64_t units_per_frame, int
   if (per_cta >= (int64_t(1) << 31) - 2 * BUILD_BLOCK)
     return set_err(OBG_EUNSUPPORTED, "too many pixels per launch (%lld units per CTA)", (long long)per_cta);
   const int grid = int((total_units + per_cta - 1) / per_cta);
+#if OBG_BUILD_RING
+  if constexpr (SMEM) {
+    if (!counts) {
+      constexpr bool BYTES = OBG_BYTE_TABLE && L == 5;
+      using P = RingPlan<L, BYTES, BUILD_BLOCK>;
+      static DevCache attr;
+      if (!attr()) {
+        CUDA_TRY(cudaFuncSetAttribute(k_build_ring<L, BYTES>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P::TOTAL)));
+        attr() = 1;
+      }
+      k_build_ring<L, BYTES><<<grid, BUILD_BLOCK, P::TOTAL, st>>>(frames, units_per_frame, total_units, group_size,
+                                                                  per_cta, ws, out_pyr, n_trees, zero_cube, zero_words,
+                                                                  levels_out);
+      LAUNCH_CHECK("k_build_ring");
+      return OBG_OK;
+    }
+  }
+#endif
 #if OBG_BYTE_TABLE
   // L = 5 only: at L = 4 uniform-random frames lose more to bank conflicts
   // of the scattered byte stores than the lookups cost (A/B: L5 -2..-5 %,
@@ -4038,8 +4345,11 @@ int obg_build_model(const uint8_t* frames, int n_frames, int height, int width, 
   if (OBG_MERGE_CSA && n_groups <= MC_MAX_TREES) {
     int64_t blocks = 1;                                   // block 0: levels 1..2
     for (int l = 3; l <= levels; ++l) blocks += (level_words(l) + MC_SLOTS - 1) / MC_SLOTS;
-    k_merge_tiles<<<dim3(unsigned(blocks), unsigned(n_regions)), MC_BLOCK, 0, st>>>(
-        static_cast<uint32_t*>(workspace), n_groups, int(n_regions), levels, k_min, out_cube, out_merged);
+    // a programmatic dependent of the build kernel just launched on `st`
+    cudaError_t le = launch_dep(k_merge_tiles, dim3(unsigned(blocks), unsigned(n_regions)), dim3(MC_BLOCK), 0, st, 1,
+                                static_cast<uint32_t*>(workspace), n_groups, int(n_regions), levels, k_min, out_cube,
+                                out_merged);
+    if (le != cudaSuccess) return set_err(OBG_ECUDA, "launch of k_merge_tiles failed: %s", cudaGetErrorString(le));
     LAUNCH_CHECK("k_merge_tiles");
   } else {
     int64_t blocks = 1;                                   // block 0: levels 1..2
@@ -4146,7 +4456,7 @@ int obg_leaf_cube(const uint32_t* pyramids, int n_trees, int levels, uint32_t* c
 
 template <int L, int OUT>
 static int launch_classify_flat(const uint8_t* frames, int64_t n_pixels, const uint32_t* cube, uint8_t* mask,
-                                unsigned long long* counts, cudaStream_t st) {
+                                unsigned long long* counts, cudaStream_t st, bool dep) {
   constexpr bool SMEM = L <= 6;
   const size_t smem = SMEM ? size_t(SmemC<L>::words) * 4 : 0;
   const int64_t n_units = n_pixels / 16;
@@ -4161,7 +4471,9 @@ static int launch_classify_flat(const uint8_t* frames, int64_t n_pixels, const u
   const int64_t need = (n_units + CLS_BLOCK - 1) / CLS_BLOCK;
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
-  k_classify_flat<L, SMEM, OUT><<<unsigned(grid), CLS_BLOCK, smem, st>>>(frames, n_units, n_pixels, cube, mask, counts);
+  cudaError_t le = launch_dep(k_classify_flat<L, SMEM, OUT>, dim3(unsigned(grid)), dim3(CLS_BLOCK), smem, st, dep ? 2 : 0, frames,
+                              n_units, n_pixels, cube, mask, counts);
+  if (le != cudaSuccess) return set_err(OBG_ECUDA, "launch of k_classify_flat failed: %s", cudaGetErrorString(le));
   LAUNCH_CHECK("k_classify_flat");
   return OBG_OK;
 }
@@ -4193,7 +4505,7 @@ static int launch_classify_l7(const uint8_t* frames, int64_t n_pixels, const uin
 template <int OUT>
 static int classify_dispatch(const uint8_t* frames, int n_frames, int height, int width, int levels, int grid_rows,
                              int grid_cols, const uint32_t* cube_bits, uint8_t* mask, unsigned long long* counts,
-                             cudaStream_t st) {
+                             cudaStream_t st, bool dep = false) {
   constexpr bool packed = OUT == OUT_PACKED || OUT == OUT_CONF_PACKED;
   const int64_t P = int64_t(height) * width;
   const int64_t n_pixels = P * n_frames;
@@ -4202,14 +4514,14 @@ static int classify_dispatch(const uint8_t* frames, int n_frames, int height, in
   const bool flat = grid_rows == 1 && grid_cols == 1 && aligned && (!packed || (P % 16) == 0);
   if (flat) {
     switch (levels) {
-      case 1: return launch_classify_flat<1, OUT>(frames, n_pixels, cube_bits, mask, counts, st);
-      case 2: return launch_classify_flat<2, OUT>(frames, n_pixels, cube_bits, mask, counts, st);
-      case 3: return launch_classify_flat<3, OUT>(frames, n_pixels, cube_bits, mask, counts, st);
-      case 4: return launch_classify_flat<4, OUT>(frames, n_pixels, cube_bits, mask, counts, st);
-      case 5: return launch_classify_flat<5, OUT>(frames, n_pixels, cube_bits, mask, counts, st);
-      case 6: return launch_classify_flat<6, OUT>(frames, n_pixels, cube_bits, mask, counts, st);
+      case 1: return launch_classify_flat<1, OUT>(frames, n_pixels, cube_bits, mask, counts, st, dep);
+      case 2: return launch_classify_flat<2, OUT>(frames, n_pixels, cube_bits, mask, counts, st, dep);
+      case 3: return launch_classify_flat<3, OUT>(frames, n_pixels, cube_bits, mask, counts, st, dep);
+      case 4: return launch_classify_flat<4, OUT>(frames, n_pixels, cube_bits, mask, counts, st, dep);
+      case 5: return launch_classify_flat<5, OUT>(frames, n_pixels, cube_bits, mask, counts, st, dep);
+      case 6: return launch_classify_flat<6, OUT>(frames, n_pixels, cube_bits, mask, counts, st, dep);
       case 7: return launch_classify_l7<OUT>(frames, n_pixels, cube_bits, mask, counts, st);
-      default: return launch_classify_flat<8, OUT>(frames, n_pixels, cube_bits, mask, counts, st);
+      default: return launch_classify_flat<8, OUT>(frames, n_pixels, cube_bits, mask, counts, st, dep);
     }
   }
   const bool band = (grid_rows > 1 || grid_cols > 1) && levels <= 6 && (width % 16) == 0 && aligned &&
@@ -4247,15 +4559,17 @@ static int classify_args(int n_frames, int height, int width, int levels, int gr
 int obg_classify(const uint8_t* frames, int n_frames, int height, int width, int levels, int grid_rows, int grid_cols,
                  const uint32_t* cube_bits, uint8_t* mask, int mask_format, void* stream) {
   g_err[0] = 0;
+  const bool dep = (mask_format & OBG_MASK_AFTER_MODEL) != 0;      // launched as a dependent of the model build
+  mask_format &= ~OBG_MASK_AFTER_MODEL;
   if (int rc = classify_args(n_frames, height, width, levels, grid_rows, grid_cols, mask_format)) return rc;
   if (n_frames == 0) return OBG_OK;
   if (!frames || !cube_bits || !mask) return set_err(OBG_EINVAL, "null buffer");
   cudaStream_t st = as_stream(stream);
   if (mask_format == OBG_MASK_PACKED)
     return classify_dispatch<OUT_PACKED>(frames, n_frames, height, width, levels, grid_rows, grid_cols, cube_bits,
-                                         mask, nullptr, st);
+                                         mask, nullptr, st, dep);
   return classify_dispatch<OUT_U8>(frames, n_frames, height, width, levels, grid_rows, grid_cols, cube_bits, mask,
-                                   nullptr, st);
+                                   nullptr, st, dep);
 }
 
 int obg_classify_confusion(const uint8_t* frames, int n_frames, int height, int width, int levels, int grid_rows,

@@ -19,8 +19,13 @@ def _check_frame_shape(model: BackgroundModel, h: int, w: int) -> None:
         raise ValueError(f"frame is {w}x{h}, model expects {model.frame_width}x{model.frame_height}")
 
 
-def classify(model: BackgroundModel, frames_dev, out=None, packed: bool = False):
+def classify(model: BackgroundModel, frames_dev, out=None, packed: bool = False, after_build: bool = False):
     """Foreground masks of a (n, h, w, 3) uint8 CUDA tensor.
+
+    ``after_build``: the previous work on the current stream is the
+    ``build_background_model_device`` call that produced ``model`` (the
+    captured step): the kernel is launched as a programmatic dependent of the
+    merge kernel (``OBG_MASK_AFTER_MODEL``), removing the launch gap.
 
     Returns (and fills ``out`` if given) a uint8 CUDA tensor: ``(n, h, w)``
     0/1 bytes, or ``(n, ceil(h*w/8))`` LSB-first bits when ``packed``.
@@ -40,7 +45,8 @@ def classify(model: BackgroundModel, frames_dev, out=None, packed: bool = False)
     lib = _lib.load()
     _lib.check(lib.obg_classify(_device.ptr(frames_dev), n, h, w, cfg.levels, cfg.grid_rows, cfg.grid_cols,
                                 _device.ptr(cube), _device.ptr(out),
-                                _lib.MASK_PACKED if packed else _lib.MASK_U8, _device.stream_handle()))
+                                (_lib.MASK_PACKED if packed else _lib.MASK_U8) |
+                                (_lib.MASK_AFTER_MODEL if after_build else 0), _device.stream_handle()))
     return out
 
 

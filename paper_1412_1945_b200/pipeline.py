@@ -57,7 +57,7 @@ class CapturedStep:
         self.step_graph = t.cuda.CUDAGraph()
         with t.cuda.graph(self.step_graph):
             self._step_bufs = build_background_model_device(train, config, workspace=self._ws_step)
-            classify(self._step_bufs, test, out=self.masks, packed=packed)
+            classify(self._step_bufs, test, out=self.masks, packed=packed, after_build=True)
         t.cuda.synchronize()
         self._last = self._view(self._build_bufs)
 
