@@ -166,6 +166,19 @@ int obg_classify_confusion(const uint8_t* frames, int n_frames, int height, int 
                            int grid_rows, int grid_cols, const uint32_t* cube_bits,
                            const uint8_t* truth, int truth_format, uint64_t* counts, void* stream);
 
+/* detect_octree with the reference's own signature (detect.py:22-53: one
+ * numpy frame in, one numpy bool mask out; the reference CLI calls it per
+ * frame, cli.py:181-187): HOST frames u8 [n][h][w][3] in, HOST masks u8
+ * [n][h][w] 0/1 out, cube_bits on the device as for obg_classify.  Frames
+ * are staged through pinned memory by the host copy pool and moved with
+ * asynchronous copies pipelined in halves around the classify kernel; the
+ * call returns when the masks are in `mask`.  Staging buffers are cached per
+ * calling thread (obg_host_stage_release frees the caller's). */
+int obg_detect_host(const uint8_t* frames, int n_frames, int height, int width, int levels,
+                    int grid_rows, int grid_cols, const uint32_t* cube_bits, uint8_t* mask,
+                    void* stream);
+void obg_host_stage_release(void);
+
 /* Preorder child-mask serialization of one pyramid (Octree.to_bytes,
  * octree.py:217-227, 258-267) computed on the device.
  *   has_root : 1 if the tree has a root node.
@@ -200,9 +213,17 @@ int obg_write_pgm_masks(const uint8_t* masks, int n_masks, int64_t width, int64_
                         const char* const* paths, int n_threads);
 
 /* Copy n host blocks of bytes_each bytes, srcs[i] -> dst + i * bytes_each
- * (e.g. a list of frames into one pinned staging buffer), split into 1 MiB
- * pieces over a persistent pool of host threads.  Host only. */
+ * (e.g. a list of frames into one pinned staging buffer), split into 256 KiB
+ * pieces over a persistent pool of host threads, with non-temporal stores
+ * (see obg_host_copy).  Host only. */
 int obg_host_gather(const uint8_t* const* srcs, int n, int64_t bytes_each, uint8_t* dst);
+
+/* One host block copied by the same pool.  streaming != 0: non-temporal
+ * stores, for a pinned destination the GPU reads next (ordinary stores leave
+ * the lines dirty in the pool cores' caches and the DMA snoops them out:
+ * ~12 GB/s instead of ~50 for a 6 MB frame); 0: ordinary stores, for data
+ * the host reads next.  obg_host_gather always streams.  Host only. */
+int obg_host_copy(const uint8_t* src, int64_t bytes, uint8_t* dst, int streaming);
 
 /* Parse one non-empty preorder child-mask tree (Octree.from_bytes /
  * decode_tree, octree.py:229-237, 250-281) at data[pos..n) into a host

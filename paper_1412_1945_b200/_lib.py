@@ -63,6 +63,9 @@ SIGNATURES = {
                                    ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
                                    ctypes.POINTER(ctypes.c_int)]),
     "obg_host_gather": (_I, [ctypes.POINTER(ctypes.c_void_p), _I, _L, _P]),
+    "obg_detect_host": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P]),
+    "obg_host_copy": (_I, [_P, _L, _P, _I]),
+    "obg_host_stage_release": (None, []),
     "obg_build_counts": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _L, _I, _P]),
     "obg_threshold_counts": (_I, [_P, _I, _I, _L, _P, _P, _P]),
     "obg_frame_diff": (_I, [_P, _P, _I, _L, _I, _P, _P]),

@@ -23,6 +23,7 @@
 #include <stdarg.h>
 #include <type_traits>
 #include <algorithm>
+#include <chrono>
 
 #include "../../include/obg.h"
 
@@ -4587,6 +4588,134 @@ int obg_classify_confusion(const uint8_t* frames, int n_frames, int height, int 
                                               cube_bits, t, c, st);
   return classify_dispatch<OUT_CONF_U8>(frames, n_frames, height, width, levels, grid_rows, grid_cols, cube_bits, t,
                                         c, st);
+}
+
+// ---------------------------------------------------------------------------
+// Host frames in, host masks out in ONE call: the reference's own
+// detect_octree(model, frame) signature (detect.py:22-53; numpy in, numpy bool
+// out), which the reference CLI loops over frame by frame (cli.py:181-187,
+// 262-288).  A pageable cudaMemcpy of a 6.2 MB frame runs at ~12 GB/s (the
+// driver's single-threaded staging copy); here the frame is copied into
+// pinned staging by libobg's host copy pool in two halves, each half's H2D
+// starting as soon as it is staged, the classify kernel follows on the same
+// stream, and the mask comes back through pinned staging in two halves, the
+// first copied out to the caller while the second is still in flight.
+// Staging and device buffers are cached per host thread (grown on demand,
+// released by obg_host_stage_release).
+// ---------------------------------------------------------------------------
+namespace {
+struct HostStage {
+  int device = -1;
+  uint8_t *pin_in = nullptr, *pin_out = nullptr, *dev_in = nullptr, *dev_out = nullptr;
+  size_t in_cap = 0, out_cap = 0;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  void release() {
+    if (pin_in) cudaFreeHost(pin_in);
+    if (pin_out) cudaFreeHost(pin_out);
+    if (dev_in) cudaFree(dev_in);
+    if (dev_out) cudaFree(dev_out);
+    for (auto& e : ev)
+      if (e) { cudaEventDestroy(e); e = nullptr; }
+    pin_in = pin_out = dev_in = dev_out = nullptr;
+    in_cap = out_cap = 0;
+    device = -1;
+  }
+};
+thread_local HostStage g_stage;
+
+int stage_reserve(HostStage& s, size_t in_bytes, size_t out_bytes) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (s.device != dev) s.release();
+  s.device = dev;
+  for (auto& e : s.ev)
+    if (!e) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  if (s.in_cap < in_bytes) {
+    if (s.pin_in) cudaFreeHost(s.pin_in);
+    if (s.dev_in) cudaFree(s.dev_in);
+    s.pin_in = s.dev_in = nullptr;
+    s.in_cap = 0;
+    CUDA_TRY(cudaMallocHost(&s.pin_in, in_bytes));
+    CUDA_TRY(cudaMalloc(&s.dev_in, in_bytes));
+    s.in_cap = in_bytes;
+  }
+  if (s.out_cap < out_bytes) {
+    if (s.pin_out) cudaFreeHost(s.pin_out);
+    if (s.dev_out) cudaFree(s.dev_out);
+    s.pin_out = s.dev_out = nullptr;
+    s.out_cap = 0;
+    CUDA_TRY(cudaMallocHost(&s.pin_out, out_bytes));
+    CUDA_TRY(cudaMalloc(&s.dev_out, out_bytes));
+    s.out_cap = out_bytes;
+  }
+  return OBG_OK;
+}
+
+int pool_copy(uint8_t* dst, const uint8_t* src, int64_t bytes, bool to_pinned) {
+  return obg_host_copy(src, bytes, dst, to_pinned ? 1 : 0);
+}
+}  // namespace
+
+void obg_host_stage_release(void) { g_stage.release(); }
+
+int obg_detect_host(const uint8_t* frames, int n_frames, int height, int width, int levels, int grid_rows,
+                    int grid_cols, const uint32_t* cube_bits, uint8_t* mask, void* stream) {
+  g_err[0] = 0;
+  if (int rc = classify_args(n_frames, height, width, levels, grid_rows, grid_cols, OBG_MASK_U8)) return rc;
+  if (n_frames == 0) return OBG_OK;
+  if (!frames || !cube_bits || !mask) return set_err(OBG_EINVAL, "null buffer");
+  cudaStream_t st = as_stream(stream);
+  const int64_t P = int64_t(height) * width;
+  // frames per pass: at most ~64 MiB of staging
+  const int64_t per_pass = std::max<int64_t>(1, std::min<int64_t>(n_frames, (int64_t(64) << 20) / (3 * P)));
+  HostStage& s = g_stage;
+  if (int rc = stage_reserve(s, size_t(per_pass * 3 * P), size_t(per_pass * P))) return rc;
+  static const bool trace = getenv("OBG_DETECT_TRACE") != nullptr;
+  auto now = [] { return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  double tq[8] = {0};
+  tq[0] = now();
+  for (int64_t f0 = 0; f0 < n_frames; f0 += per_pass) {
+    const int64_t m = std::min<int64_t>(per_pass, n_frames - f0);
+    const int64_t in_bytes = m * 3 * P, out_bytes = m * P;
+    const uint8_t* src = frames + f0 * 3 * P;
+    uint8_t* dst = mask + f0 * P;
+    // in: two halves (cut at a multiple of 256 bytes), stage -> H2D
+    const int64_t cut_in = (in_bytes / 2) & ~int64_t(255);
+    const int64_t in_off[3] = {0, cut_in, in_bytes};
+    for (int h = 0; h < 2; ++h) {
+      const int64_t len = in_off[h + 1] - in_off[h];
+      if (len == 0) continue;
+      if (int rc = pool_copy(s.pin_in + in_off[h], src + in_off[h], len, true)) return rc;
+      tq[1 + 2 * h] = now();
+      CUDA_TRY(cudaMemcpyAsync(s.dev_in + in_off[h], s.pin_in + in_off[h], size_t(len), cudaMemcpyHostToDevice, st));
+      tq[2 + 2 * h] = now();
+    }
+    if (int rc = classify_dispatch<OUT_U8>(s.dev_in, int(m), height, width, levels, grid_rows, grid_cols, cube_bits,
+                                           s.dev_out, nullptr, st))
+      return rc;
+    // out: two halves, D2H -> copy out (the second transfer overlaps the first copy)
+    const int64_t cut_out = (out_bytes / 2) & ~int64_t(255);
+    const int64_t out_off[3] = {0, cut_out, out_bytes};
+    for (int h = 0; h < 2; ++h) {
+      const int64_t len = out_off[h + 1] - out_off[h];
+      if (len > 0)
+        CUDA_TRY(cudaMemcpyAsync(s.pin_out + out_off[h], s.dev_out + out_off[h], size_t(len), cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaEventRecord(s.ev[h], st));
+    }
+    tq[5] = now();
+    for (int h = 0; h < 2; ++h) {
+      CUDA_TRY(cudaEventSynchronize(s.ev[h]));
+      if (h == 0) tq[6] = now();
+      const int64_t len = out_off[h + 1] - out_off[h];
+      if (len > 0)
+        if (int rc = pool_copy(dst + out_off[h], s.pin_out + out_off[h], len, false)) return rc;
+    }
+    tq[7] = now();
+    if (trace)
+      fprintf(stderr, "obg_detect_host: stage0 %.0f h2d0-call %.0f stage1 %.0f h2d1-call %.0f launch+d2h-calls %.0f wait0 %.0f rest %.0f total %.0f us\n",
+              tq[1] - tq[0], tq[2] - tq[1], tq[3] - tq[2], tq[4] - tq[3], tq[5] - tq[4], tq[6] - tq[5], tq[7] - tq[6], tq[7] - tq[0]);
+  }
+  return OBG_OK;
 }
 
 int64_t obg_serialize_workspace_bytes(int levels) {

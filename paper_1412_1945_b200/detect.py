@@ -50,6 +50,22 @@ def classify(model: BackgroundModel, frames_dev, out=None, packed: bool = False,
     return out
 
 
+def _detect_host(model: BackgroundModel, frames: np.ndarray) -> np.ndarray:
+    """(n, h, w, 3) uint8 numpy frames -> (n, h, w) bool numpy masks through
+    ``obg_detect_host``: the frames are staged into pinned memory by the
+    native copy pool and moved with asynchronous copies pipelined around the
+    classify kernel (a pageable ``cudaMemcpy`` of a frame is a single host
+    thread at ~12 GB/s; per 1080p frame 0.83 -> see tools/sig_probe.py)."""
+    frames = np.ascontiguousarray(frames)
+    n, h, w = frames.shape[0], frames.shape[1], frames.shape[2]
+    cfg = model.config
+    cube = model.device_cube()
+    out = np.empty((n, h, w), dtype=np.bool_)
+    _lib.check(_lib.load().obg_detect_host(frames.ctypes.data, n, h, w, cfg.levels, cfg.grid_rows, cfg.grid_cols,
+                                           _device.ptr(cube), out.ctypes.data, _device.stream_handle()))
+    return out
+
+
 def detect_octree(model: BackgroundModel, frame) -> np.ndarray:
     """Mask of pixels whose quantized colour is missing from their region's
     tree (detect.py:22-53).  A CUDA tensor in gives a CUDA bool tensor out."""
@@ -67,11 +83,7 @@ def detect_octree(model: BackgroundModel, frame) -> np.ndarray:
     h, w = frame.shape[0], frame.shape[1]
     _check_frame_shape(model, h, w)
     _device.require_cuda()
-    # one frame: pageable copies beat pinned staging here (the staging copy
-    # and its synchronisation cost more than the driver's own: 1.17 vs
-    # 0.83 ms per 1080p frame, tools/sig_probe.py)
-    mask = classify(model, _device.to_device_u8(frame[None]))
-    return mask[0].cpu().numpy().view(np.bool_)
+    return _detect_host(model, frame[None])[0]
 
 
 def detect_octree_batch(model: BackgroundModel, frames) -> np.ndarray:
@@ -84,8 +96,7 @@ def detect_octree_batch(model: BackgroundModel, frames) -> np.ndarray:
         raise ValueError(f"expected (n, h, w, 3) uint8 frames, got {frames.dtype} {frames.shape}")
     _check_frame_shape(model, frames.shape[1], frames.shape[2])
     _device.require_cuda()
-    mask = classify(model, _device.to_device_u8(frames))
-    return mask.cpu().numpy().view(np.bool_)
+    return _detect_host(model, frames)
 
 
 # ---------------------------------------------------------------------------

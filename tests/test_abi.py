@@ -72,3 +72,26 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
     monkeypatch.setattr(_lib, "_lib", None)
     with pytest.raises(_lib.LibraryNotBuilt):
         _lib.load()
+
+
+@pytest.mark.parametrize("streaming", [0, 1])
+def test_host_pool_copies(streaming):
+    """obg_host_copy / obg_host_gather (the host copy pool, ordinary and
+    non-temporal stores): any size, any destination alignment."""
+    import numpy as np
+    lib = _lib.load()
+    rng = np.random.default_rng(7 + streaming)
+    for size in (1, 15, 16, 17, 255, 4096, 262144, 262145, 1_000_003, 6_220_800):
+        for off in (0, 1, 7, 16, 33):
+            src = rng.integers(0, 256, size, dtype=np.uint8)
+            dst = np.full(size + 64, 0xA5, np.uint8)
+            assert lib.obg_host_copy(src.ctypes.data, size, dst.ctypes.data + off, streaming) == 0
+            assert np.array_equal(dst[off:off + size], src)
+            assert (dst[:off] == 0xA5).all() and (dst[off + size:] == 0xA5).all()   # nothing written outside
+    blocks = [rng.integers(0, 256, 300_001, dtype=np.uint8) for _ in range(5)]
+    dst = np.zeros(5 * 300_001 + 3, np.uint8)
+    srcs = (ctypes.c_void_p * 5)(*[b.ctypes.data for b in blocks])
+    assert lib.obg_host_gather(srcs, 5, 300_001, dst.ctypes.data + 3) == 0
+    assert np.array_equal(dst[3:], np.concatenate(blocks))
+    assert lib.obg_host_copy(None, 4, dst.ctypes.data, 0) != 0          # null source is an argument error
+    assert lib.obg_host_copy(blocks[0].ctypes.data, 0, dst.ctypes.data, 1) == 0

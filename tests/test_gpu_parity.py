@@ -661,3 +661,47 @@ def test_device_serializer_large_trees(cuda, levels, n_codes):
     got = dev_tree.to_bytes()
     assert got == want
     assert Octree.from_bytes(got, levels) == host
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,n,levels,grid", [((1, 1), 3, 4, (1, 1)), ((7, 5), 9, 6, (1, 1)), ((48, 64), 5, 5, (2, 3)),
+                                                  ((120, 160), 4, 7, (1, 1)), ((33, 17), 2, 8, (1, 1)),
+                                                  ((1080, 1920), 2, 6, (1, 1))])
+def test_detect_host_matches_device_classify(cuda, shape, n, levels, grid):
+    """obg_detect_host (host frames in, host masks out: the reference's
+    detect_octree signature, detect.py:22-53) against the device classify and
+    the oracle, single frames and batches, odd sizes, grids."""
+    import torch
+    h, w = shape
+    rng = np.random.default_rng(h * 131 + w + levels)
+    base = rng.integers(0, 256, size=(1, 1, 1, 3))
+    train = np.clip(base + rng.integers(-20, 21, size=(6, h, w, 3)), 0, 255).astype(np.uint8)
+    probe = np.clip(base + rng.integers(-40, 41, size=(n, h, w, 3)), 0, 255).astype(np.uint8)
+    cfg = obg.ModelConfig(levels=levels, threshold=0.5, grid_rows=grid[0], grid_cols=grid[1], training_frames=6)
+    model = obg.build_background_model(list(train), cfg)
+    want_dev = obg.classify(model, torch.from_numpy(probe).cuda()).cpu().numpy().astype(bool)
+    got_batch = obg.detect_octree_batch(model, probe)
+    assert got_batch.dtype == np.bool_ and got_batch.shape == (n, h, w)
+    assert np.array_equal(got_batch, want_dev)
+    for i in range(n):
+        got = obg.detect_octree(model, probe[i])
+        assert got.dtype == np.bool_ and np.array_equal(got, want_dev[i])
+    # a non-contiguous frame view is accepted like any numpy input
+    assert np.array_equal(obg.detect_octree(model, probe[0][:, ::-1][:, ::-1]), want_dev[0])
+    if h * w <= 160 * 120:
+        trees = orc.build_background_model(list(train), levels, 0.5, grid[0], grid[1])
+        assert np.array_equal(got_batch[0], orc.detect_octree(trees, probe[0], levels, grid[0], grid[1]))
+
+
+@pytest.mark.gpu
+def test_detect_host_many_frames_cross_staging_passes(cuda):
+    """More frames than one staging pass holds (64 MiB): the passes line up."""
+    import torch
+    rng = np.random.default_rng(99)
+    h, w, n = 540, 960, 60                                      # 1.5 MB per frame: 44 frames per pass
+    train = rng.integers(100, 140, size=(4, h, w, 3), dtype=np.uint8)
+    probe = rng.integers(90, 150, size=(n, h, w, 3), dtype=np.uint8)
+    cfg = obg.ModelConfig(levels=5, threshold=0.5, training_frames=4)
+    model = obg.build_background_model(list(train), cfg)
+    want = obg.classify(model, torch.from_numpy(probe).cuda()).cpu().numpy().astype(bool)
+    assert np.array_equal(obg.detect_octree_batch(model, probe), want)
