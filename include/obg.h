@@ -24,7 +24,9 @@
  *   cube     u32 [obg_cube_words(L)]           classify operand: leaf bitset in
  *            "RGB cube" order, idx = R'<<2L | G'<<L | B' with C' = C >> (8-L)
  *            (max(1, 8^L/32) words); for L = 7 followed by a 2-bit state per
- *            L=6 cell (16384 words: some / all of its 8 leaves present).
+ *            L=6 cell (16384 words: some / all of its 8 leaves present), 32
+ *            words of cell counts and the L=6 bitset of full cells (8192
+ *            words) -- what the L = 7 classify picks its kernel by.
  *   mask     u8  [n_frames][height][width]     0/1 (numpy bool layout), or
  *            bit-packed u8 [n_frames][ceil(h*w/8)], LSB-first per frame.
  */

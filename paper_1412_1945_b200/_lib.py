@@ -71,7 +71,7 @@ SIGNATURES = {
     "obg_frame_diff": (_I, [_P, _P, _I, _L, _I, _P, _P]),
     "obg_running_average": (_I, [_P, _I, _L, _L, _P, _I, _P, _P]),
 }
-ABI_VERSION = 7
+ABI_VERSION = 8
 
 
 class LibraryNotBuilt(RuntimeError):
@@ -140,6 +140,7 @@ def level_offset(level: int) -> int:
 
 def cube_words(levels: int) -> int:
     """Words of one region's classify operand: the leaf cube, plus for L = 7
-    a 2-bit state per L=6 cell (16384 words) and 32 words of cell counts
-    (k_l7_states; the L7 classify picks its path by them)."""
-    return level_words(levels) + (16384 + 32 if levels == 7 else 0)
+    a 2-bit state per L=6 cell (16384 words), 32 words of cell counts
+    (k_l7_states; the L7 classify picks its path by them) and one bit per
+    L=6 cell whose 8 leaves are all present (8192 words)."""
+    return level_words(levels) + (16384 + 32 + 8192 if levels == 7 else 0)

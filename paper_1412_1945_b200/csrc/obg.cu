@@ -27,7 +27,7 @@
 
 #include "../../include/obg.h"
 
-#define OBG_ABI_VERSION 7
+#define OBG_ABI_VERSION 8
 #define OBG_CUBE_ZEROED 0x100   /* internal: out_cube already cleared by the build kernel */
 
 // ---------------------------------------------------------------------------
@@ -140,10 +140,16 @@ __host__ __device__ static constexpr int64_t cube_words(int L) { return level_wo
 // Classify operand per region: the leaf cube, plus for L = 7 a 2-bit state
 // per L=6 cell (16384 words, see k_classify_l7).
 constexpr int64_t S7_CANON_WORDS = 16384;
+// (+ S7_CELL_WORDS after the counts: one bit per L=6 cell whose 8 leaves are
+// all present, in L=6 cube order -- the operand of the L=6 classify kernel
+// that answers for a model without partly filled cells)
+constexpr int64_t S7_CELL_WORDS = 8192;
+constexpr int64_t S7_COUNTS_OFF = 65536 + S7_CANON_WORDS;          // cube_words(7) + states
+constexpr int64_t S7_CELLS_OFF = S7_COUNTS_OFF + 32;
 // (+ 32 words: [0] = cells with some but not all leaves, [1] = cells with
 // any leaf -- what k_classify_l7 picks its lookup path by)
 __host__ __device__ static constexpr int64_t operand_words(int L) {
-  return cube_words(L) + (L == 7 ? S7_CANON_WORDS + 32 : 0);
+  return cube_words(L) + (L == 7 ? S7_CANON_WORDS + 32 + S7_CELL_WORDS : 0);
 }
 
 // Build workspace per tree: the leaf cube, then levels 1..L-1 in cube order
@@ -2693,15 +2699,28 @@ __global__ void __launch_bounds__(1024) k_l7_states(uint32_t* __restrict__ opera
   __shared__ uint32_t s_red[2][32];
   uint32_t* op = operand + int64_t(blockIdx.x) * operand_words(7);
   uint32_t mixed = 0, some = 0;
-  for (uint32_t i = threadIdx.x; i < uint32_t(S7_CANON_WORDS); i += 1024) {
-    const uint32_t r6 = i >> 8, g6 = (i >> 2) & 63u, q = i & 3u;
-    const uint32_t b = (2u * r6) * 512u + (2u * g6) * 4u + q;
-    const uint32_t w00 = op[b], w01 = op[b + 4], w10 = op[b + 512], w11 = op[b + 516];
-    const uint32_t a = w00 | w01 | w10 | w11, A = w00 & w01 & w10 & w11;
-    const uint32_t sm = (a | (a >> 1)) & 0x55555555u, al = (A & (A >> 1)) & 0x55555555u;
-    op[cube_words(7) + i] = sm | (al << 1);
-    some += __popc(sm);
-    mixed += __popc(sm & ~al);
+  // one thread per full-cell word = two state words (B6 = 0..15 | 16..31 of a half row)
+  for (uint32_t j = threadIdx.x; j < uint32_t(S7_CELL_WORDS); j += 1024) {
+    uint32_t cells = 0;
+#pragma unroll
+    for (uint32_t hq = 0; hq < 2; ++hq) {
+      const uint32_t i = 2u * j + hq;
+      const uint32_t r6 = i >> 8, g6 = (i >> 2) & 63u, q = i & 3u;
+      const uint32_t b = (2u * r6) * 512u + (2u * g6) * 4u + q;
+      const uint32_t w00 = op[b], w01 = op[b + 4], w10 = op[b + 512], w11 = op[b + 516];
+      const uint32_t a = w00 | w01 | w10 | w11, A = w00 & w01 & w10 & w11;
+      const uint32_t sm = (a | (a >> 1)) & 0x55555555u, al = (A & (A >> 1)) & 0x55555555u;
+      op[cube_words(7) + i] = sm | (al << 1);
+      some += __popc(sm);
+      mixed += __popc(sm & ~al);
+      uint32_t x = al;                                           // even bits -> low 16 bits
+      x = (x | (x >> 1)) & 0x33333333u;
+      x = (x | (x >> 2)) & 0x0F0F0F0Fu;
+      x = (x | (x >> 4)) & 0x00FF00FFu;
+      x = (x | (x >> 8)) & 0x0000FFFFu;
+      cells |= x << (16u * hq);
+    }
+    op[S7_CELLS_OFF + j] = cells;                                // L=6 cube word (R6 << 7 | G6 << 1 | B6 >> 5)
   }
   mixed = __reduce_add_sync(0xFFFFFFFFu, mixed);
   some = __reduce_add_sync(0xFFFFFFFFu, some);
@@ -2714,7 +2733,7 @@ __global__ void __launch_bounds__(1024) k_l7_states(uint32_t* __restrict__ opera
     mixed = __reduce_add_sync(0xFFFFFFFFu, s_red[0][threadIdx.x]);
     some = __reduce_add_sync(0xFFFFFFFFu, s_red[1][threadIdx.x]);
     // the operand's 32-word tail: [0] mixed, [1] occupied, the rest zero
-    op[cube_words(7) + S7_CANON_WORDS + threadIdx.x] = threadIdx.x == 0 ? mixed : threadIdx.x == 1 ? some : 0u;
+    op[S7_COUNTS_OFF + threadIdx.x] = threadIdx.x == 0 ? mixed : threadIdx.x == 1 ? some : 0u;
   }
 }
 
@@ -2852,7 +2871,11 @@ template <int L, bool SMEM_BITS, int OUT>
 #endif
 __global__ void __launch_bounds__(CLS_BLOCK, OBG_CLS_MINB)
 k_classify_flat(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_pixels,
-                const uint32_t* __restrict__ cube, uint8_t* __restrict__ mask, unsigned long long* counts) {
+                const uint32_t* __restrict__ cube, uint8_t* __restrict__ mask, unsigned long long* counts,
+                const uint32_t* __restrict__ gate) {
+  // gate (L = 7 models classified through their L = 6 full-cell bitset):
+  // the count of partly filled cells; this launch answers only when it is 0
+  if (gate != nullptr && __ldg(gate) != 0u) return;
   ConfAcc acc;
   extern __shared__ uint32_t s_bits[];
   constexpr int64_t CW = cube_words(L);
@@ -3156,17 +3179,23 @@ __device__ __forceinline__ void classify_l7_cube(const uint8_t* __restrict__ fra
 //  * otherwise the cube in shared memory, one direct lookup per pixel (a
 //    half-full model 0.96 -> 0.36 ms; C3-like scene at L7 0.15 -> 0.125 ms;
 //    a 15 %-mixed model on uniform frames 0.47 -> 0.19 ms).
-__device__ __forceinline__ bool l7_direct(const uint32_t* __restrict__ operand) {
-  const uint32_t mixed = __ldg(operand + cube_words(7) + S7_CANON_WORDS);
-  const uint32_t some = __ldg(operand + cube_words(7) + S7_CANON_WORDS + 1);
-  return OBG_L7_PATH == 2 || (OBG_L7_PATH == 0 && 32u * mixed >= some && mixed > 0);
+// 0: state table, 1: cube in shared memory, 2: no partly filled cell -- the
+// L=6 kernel on the full-cell bitset answers (k_classify_flat<6> with a gate)
+#ifndef OBG_L7_CELLS
+#define OBG_L7_CELLS 1
+#endif
+__device__ __forceinline__ int l7_path(const uint32_t* __restrict__ operand) {
+  const uint32_t mixed = __ldg(operand + S7_COUNTS_OFF);
+  const uint32_t some = __ldg(operand + S7_COUNTS_OFF + 1);
+  if (OBG_L7_PATH == 0 && OBG_L7_CELLS && mixed == 0) return 2;
+  return (OBG_L7_PATH == 2 || (OBG_L7_PATH == 0 && 32u * mixed >= some && mixed > 0)) ? 1 : 0;
 }
 static_assert(S7_BLOCK == C7_BLOCK, "one block size for both L7 paths");
 template <int OUT, bool DIRECT>
 __global__ void __launch_bounds__(C7_BLOCK, 1)
 k_classify_l7(const uint8_t* __restrict__ frames, int64_t n_units, int64_t n_pixels, const uint32_t* __restrict__ cube,
               uint8_t* __restrict__ mask, unsigned long long* counts) {
-  if (l7_direct(cube) != DIRECT) return;
+  if (l7_path(cube) != (DIRECT ? 1 : 0)) return;
   ConfAcc acc;
   extern __shared__ __align__(16) uint32_t s_dyn[];
   if constexpr (DIRECT) classify_l7_cube<OUT>(frames, n_units, n_pixels, cube, mask, acc, s_dyn);
@@ -4457,7 +4486,7 @@ int obg_leaf_cube(const uint32_t* pyramids, int n_trees, int levels, uint32_t* c
 
 template <int L, int OUT>
 static int launch_classify_flat(const uint8_t* frames, int64_t n_pixels, const uint32_t* cube, uint8_t* mask,
-                                unsigned long long* counts, cudaStream_t st, bool dep) {
+                                unsigned long long* counts, cudaStream_t st, bool dep, const uint32_t* gate = nullptr) {
   constexpr bool SMEM = L <= 6;
   const size_t smem = SMEM ? size_t(SmemC<L>::words) * 4 : 0;
   const int64_t n_units = n_pixels / 16;
@@ -4473,7 +4502,7 @@ static int launch_classify_flat(const uint8_t* frames, int64_t n_pixels, const u
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
   cudaError_t le = launch_dep(k_classify_flat<L, SMEM, OUT>, dim3(unsigned(grid)), dim3(CLS_BLOCK), smem, st, dep ? 2 : 0, frames,
-                              n_units, n_pixels, cube, mask, counts);
+                              n_units, n_pixels, cube, mask, counts, gate);
   if (le != cudaSuccess) return set_err(OBG_ECUDA, "launch of k_classify_flat failed: %s", cudaGetErrorString(le));
   LAUNCH_CHECK("k_classify_flat");
   return OBG_OK;
@@ -4498,7 +4527,14 @@ static int launch_classify_l7(const uint8_t* frames, int64_t n_pixels, const uin
   LAUNCH_CHECK("k_classify_l7<states>");
   k_classify_l7<OUT, true><<<unsigned(grid), C7_BLOCK, smem_c, st>>>(frames, n_units, n_pixels, cube, mask, counts);
   LAUNCH_CHECK("k_classify_l7<cube>");
+#if OBG_L7_CELLS
+  // third candidate: every occupied L=6 cell is full, so the L=6 kernel on the
+  // full-cell bitset gives the same masks at the L=6 kernel's speed
+  return launch_classify_flat<6, OUT>(frames, n_pixels, cube + S7_CELLS_OFF, mask, counts, st, false,
+                                      cube + S7_COUNTS_OFF);
+#else
   return OBG_OK;
+#endif
 }
 
 // obg_classify / obg_classify_confusion: `mask` is the output mask or the

@@ -705,3 +705,51 @@ def test_detect_host_many_frames_cross_staging_passes(cuda):
     model = obg.build_background_model(list(train), cfg)
     want = obg.classify(model, torch.from_numpy(probe).cuda()).cpu().numpy().astype(bool)
     assert np.array_equal(obg.detect_octree_batch(model, probe), want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n_cells,drop", [(300, 0), (300, 1), (0, 0), (4000, 0)])
+def test_l7_full_cell_models(cuda, n_cells, drop):
+    """L = 7 models whose occupied L=6 cells hold all 8 leaves classify through
+    the L=6 kernel on the full-cell bitset (k_l7_states' third operand part);
+    dropping one leaf (drop=1) makes a cell partial and must fall back to the
+    L=7 kernels.  Checked against the oracle and against a host-side bit test."""
+    import torch
+    rng = np.random.default_rng(1000 + n_cells + drop)
+    h, w = 192, 256
+    cells = rng.choice(1 << 18, size=n_cells, replace=False)
+    r6, g6, b6 = (cells >> 12) & 63, (cells >> 6) & 63, cells & 63
+    leaves = []
+    for d in range(8):                                           # all 8 children of each cell
+        leaves.append(np.stack([(2 * r6 + (d >> 2)) << 1, (2 * g6 + ((d >> 1) & 1)) << 1, (2 * b6 + (d & 1)) << 1], 1))
+    px = np.concatenate(leaves).astype(np.uint8) if n_cells else np.zeros((0, 3), np.uint8)
+    if drop and len(px):
+        px = px[1:]                                              # one leaf missing: its cell is partial
+    frame = np.zeros((h, w, 3), np.uint8)
+    flat = frame.reshape(-1, 3)
+    if len(px):
+        reps = -(-flat.shape[0] // len(px))
+        flat[:] = np.tile(px, (reps, 1))[:flat.shape[0]]
+    else:
+        flat[:] = (1, 1, 1)                                      # a single leaf: one partial cell -> not the cells path
+    train = np.stack([frame, frame])
+    cfg = obg.ModelConfig(levels=7, threshold=0.5, training_frames=2)
+    model = obg.build_background_model(list(train), cfg)
+    probe = rng.integers(0, 256, size=(3, h, w, 3), dtype=np.uint8)
+    probe[0].reshape(-1, 3)[:len(flat) // 2] = flat[:len(flat) // 2] ^ rng.integers(0, 2, size=(len(flat) // 2, 3), dtype=np.uint8)
+    probe[1] = frame
+    got = obg.classify(model, torch.from_numpy(probe).cuda()).cpu().numpy().astype(bool)
+    # host-side truth: a pixel is background iff its 7-bit colour is a training colour
+    key = lambda a: (a[..., 0].astype(np.int64) >> 1) << 14 | (a[..., 1].astype(np.int64) >> 1) << 7 | (a[..., 2].astype(np.int64) >> 1)
+    present = np.zeros(1 << 21, bool)
+    present[key(flat)] = True
+    assert np.array_equal(got, ~present[key(probe)])
+    assert not got[1].any()
+    trees = orc.build_background_model(list(train), 7, 0.5, 1, 1)
+    assert np.array_equal(got[2], orc.detect_octree(trees, probe[2], 7, 1, 1))
+    # the same model loaded from its bytes (host tree -> obg_leaf_cube -> k_l7_states)
+    loaded = obg.read_model(obg.write_model(model))
+    assert np.array_equal(obg.detect_octree_batch(loaded, probe), got)
+    # bit-packed output takes the same path
+    packed = obg.classify(model, torch.from_numpy(probe).cuda(), packed=True).cpu().numpy()
+    assert np.array_equal(np.unpackbits(packed, axis=1, bitorder="little")[:, :h * w].reshape(3, h, w).astype(bool), got)
