@@ -3927,6 +3927,135 @@ k_hist(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t tota
   }
 }
 
+// ---------------------------------------------------------------------------
+// a13 at L = 6: a per-CTA HASHED shared-memory histogram.  8^6 u32 bins are
+// 1 MB, four times shared memory, but a CTA's range of a natural scene touches
+// only a few thousand leaves (C3: ~4 k of 262 144 per CTA segment), so the
+// private histogram is an open-addressing table of 2^14 (key, count) slots
+// (128 KB): a pixel run looks its leaf up (linear probing from a
+// multiplicative hash, at most HH_PROBES slots), claims an empty slot with one
+// atomicCAS the first time, and adds with one shared atomic.  What does not
+// fit goes straight to the tree's counts in global memory, exactly as the
+// unhashed path does (the total is the same whichever way an add goes); when a
+// segment has sent HH_GIVE_UP adds that way (uniform-random frames fill the
+// table in the first 1 % of a segment) the CTA stops probing for the rest of
+// the segment.  At a segment end the table is flushed to the path-order counts
+// and cleared.  A thread's 16 consecutive pixels are run-length merged first,
+// and a warp whose lanes all add to one leaf (single-colour frames) reduces
+// to one add, as in the global path.
+// ---------------------------------------------------------------------------
+#ifndef OBG_HIST_HASH
+#define OBG_HIST_HASH 1
+#endif
+constexpr uint32_t HH_LOG = 14, HH_SLOTS = 1u << HH_LOG, HH_EMPTY = 0xFFFFFFFFu;
+constexpr int HH_PROBES = 6;
+constexpr uint32_t HH_GIVE_UP = 4096;
+
+// one add of `cnt` to leaf `idx` (cube order); returns false if the table had no room
+__device__ __forceinline__ bool hh_add(uint32_t* keys, uint32_t* cnts, uint32_t idx, uint32_t cnt) {
+  uint32_t h = (idx * 0x9E3779B1u) >> (32 - HH_LOG);
+#pragma unroll 1
+  for (int p = 0; p < HH_PROBES; ++p) {
+    uint32_t k = keys[h];
+    if (k == HH_EMPTY) k = atomicCAS(keys + h, HH_EMPTY, idx);     // returns the old key: EMPTY = claimed
+    if (k == idx || k == HH_EMPTY) {
+      atomicAdd(cnts + h, cnt);
+      return true;
+    }
+    h = (h + 1u) & (HH_SLOTS - 1u);
+  }
+  return false;
+}
+
+template <int L>
+__global__ void __launch_bounds__(HIST_BLOCK, 1)
+k_hist_hash(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t total_units, int group_size,
+            int64_t units_per_cta, uint32_t* __restrict__ counts) {
+  extern __shared__ __align__(16) uint32_t s_hh[];
+  uint32_t* keys = s_hh;
+  uint32_t* cnts = s_hh + HH_SLOTS;
+  uint32_t* s_spill = s_hh + 2 * HH_SLOTS;             // adds of this segment that went to global memory
+  constexpr int64_t NB = int64_t(1) << (3 * L);
+  const int64_t u_begin = int64_t(blockIdx.x) * units_per_cta;
+  const int64_t u_end = min(total_units, u_begin + units_per_cta);
+  if (u_begin >= u_end) return;
+  for (uint32_t i = threadIdx.x; i < HH_SLOTS; i += HIST_BLOCK) {
+    keys[i] = HH_EMPTY;
+    cnts[i] = 0u;
+  }
+  if (threadIdx.x == 0) *s_spill = 0u;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t upt = units_per_frame * group_size;
+  int64_t u = u_begin;
+  while (u < u_end) {
+    const int64_t tree = u / upt;
+    const int64_t seg_end = min(u_end, (tree + 1) * upt);
+    uint32_t* dst = counts + tree * NB;
+    const int64_t seg_len = seg_end - u;
+    const int32_t rel0 = int32_t(threadIdx.x) - lane;
+    const int32_t n_it = seg_len > rel0 ? int32_t((seg_len - rel0 + HIST_BLOCK - 1) / HIST_BLOCK) : 0;
+    const int32_t n_lane = seg_len > rel0 + lane ? int32_t((seg_len - rel0 - lane + HIST_BLOCK - 1) / HIST_BLOCK) : 0;
+    constexpr int64_t STEP = 48 * int64_t(HIST_BLOCK);
+    const uint8_t* fp = frames + 48 * (u + rel0 + lane);
+    // one run of `run` pixels of leaf `idx` (`go` = this lane has one)
+    auto add_run = [&](uint32_t idx, uint32_t run, bool go, bool hashed) {
+      if (go) {
+        if (!(hashed && hh_add(keys, cnts, idx, run))) {
+          atomicAdd(dst + cube_to_code(idx, L), run);
+          if (hashed) atomicAdd(s_spill, 1u);
+        }
+      }
+    };
+    auto unit = [&](const uint32_t (&w)[12], bool valid) {
+      const bool hashed = *reinterpret_cast<volatile uint32_t*>(s_spill) < HH_GIVE_UP;
+      uint32_t prev = 0, run = 0;
+      for16([&](auto jc) {
+        constexpr int j = decltype(jc)::value;
+        const uint32_t idx = cube_idx<L>(pixel_word<j>(w));
+        if constexpr (j == 0) {
+          prev = idx;
+          run = 1;
+        } else {
+          const bool change = idx != prev;
+          add_run(prev, run, valid && change, hashed);
+          run = change ? 1u : run + 1u;
+          prev = idx;
+        }
+      });
+      // the unit's last run; when every lane's whole unit is one run of one
+      // leaf (single-colour frames) the warp reduces to a single add
+      const uint32_t i0 = __shfl_sync(0xFFFFFFFFu, prev, 0);
+      const bool one = __all_sync(0xFFFFFFFFu, valid && run == 16u && prev == i0);
+      add_run(prev, one ? 16u * 32u : run, one ? lane == 0 : valid, hashed);
+    };
+    uint32_t wa[12], wb[12];
+    if (0 < n_lane) load_unit_at(fp, wa);
+    for (int32_t k = 0; k < n_it;) {
+      if (k + 1 < n_lane) load_unit_at(fp + STEP, wb);
+      unit(wa, k < n_lane);
+      fp += STEP;
+      if (++k >= n_it) break;
+      if (k + 1 < n_lane) load_unit_at(fp + STEP, wa);
+      unit(wb, k < n_lane);
+      fp += STEP;
+      ++k;
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < HH_SLOTS; i += HIST_BLOCK) {
+      const uint32_t k = keys[i];
+      if (k != HH_EMPTY) {
+        atomicAdd(dst + cube_to_code(k, L), cnts[i]);
+        keys[i] = HH_EMPTY;
+        cnts[i] = 0u;
+      }
+    }
+    if (threadIdx.x == 0) *s_spill = 0u;
+    __syncthreads();
+    u = seg_end;
+  }
+}
+
 // (A/B variant, OBG_HIST_CLUSTER=1; slower than the global atomics, see above)
 // L = 6: the 8^6-bin u32 histogram (1 MB) is privatised per CLUSTER of 8 CTAs
 // in distributed shared memory -- each CTA holds 1/8 of the bins (128 KB) and
@@ -4161,6 +4290,23 @@ static int launch_hist(const uint8_t* frames, int64_t units_per_frame, int64_t t
     if (OBG_HIST_CLUSTER == 2) return launch_hist_slices(frames, units_per_frame, total_units, group_size, counts, st);
   }
   constexpr bool SMEM = L <= 5;
+  if constexpr (L == 6 && OBG_HIST_HASH) {      // L >= 7: a CTA segment of a natural scene overflows the table (A/B: C3 scene at L7 +50 %)
+    constexpr size_t smem_h = (2 * size_t(HH_SLOTS) + 4) * 4;
+    static DevCache attr_h;
+    if (!attr_h()) {
+      CUDA_TRY(cudaFuncSetAttribute(k_hist_hash<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_h)));
+      attr_h() = 1;
+    }
+    const int64_t upt = units_per_frame * group_size;
+    const int64_t per_h = choose_units_per_cta(total_units, upt, total_units / upt, sm_count(), HIST_BLOCK);
+    if (per_h >= (int64_t(1) << 31) - 2 * HIST_BLOCK)
+      return set_err(OBG_EUNSUPPORTED, "too many pixels per launch (%lld units per CTA)", (long long)per_h);
+    k_hist_hash<L><<<int((total_units + per_h - 1) / per_h), HIST_BLOCK, smem_h, st>>>(frames, units_per_frame,
+                                                                                      total_units, group_size, per_h,
+                                                                                      counts);
+    LAUNCH_CHECK("k_hist_hash");
+    return OBG_OK;
+  }
   const size_t smem = SMEM ? (size_t(1) << (3 * L)) * 4 : 0;
   static DevCache attr;
   if (!attr()) {
