@@ -287,12 +287,18 @@ def build_frame_tree(frames, region: tuple[int, int], config: ModelConfig) -> Oc
         raise ValueError(f"region {region} outside {config.grid_rows}x{config.grid_cols} grid")
     rows = region_bounds(h, config.grid_rows)
     cols = region_bounds(w, config.grid_cols)
-    blocks = np.stack([f[rows[row]:rows[row + 1], cols[col]:cols[col + 1]] for f in frames])
-    if blocks.shape[1] == 0 or blocks.shape[2] == 0:
-        return Octree(config.levels)
     from . import _device
-    _device.require_cuda()
-    dev = _device.to_device_u8(blocks)
+    if (rows[row], rows[row + 1], cols[col], cols[col + 1]) == (0, h, 0, w) and h * w > 0:
+        # the region is the whole frame (1x1 grids): no block copy, the frames
+        # go up through pinned staging (pool gather + asynchronous H2D)
+        _device.require_cuda()
+        dev = _device.frames_list_to_device(frames)
+    else:
+        blocks = np.stack([f[rows[row]:rows[row + 1], cols[col]:cols[col + 1]] for f in frames])
+        if blocks.shape[1] == 0 or blocks.shape[2] == 0:
+            return Octree(config.levels)
+        _device.require_cuda()
+        dev = _device.to_device_u8(blocks)
     pyr = build_presence(dev, config.levels, 1, 1, len(frames))
     return Octree._from_device(pyr[0, 0], config.levels)
 
