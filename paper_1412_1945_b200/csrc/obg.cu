@@ -3947,12 +3947,46 @@ k_hist(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t tota
 #ifndef OBG_HIST_HASH
 #define OBG_HIST_HASH 1
 #endif
+#ifdef OBG_HH_BUCKETS
+#define OBG_HH_BUCKETS_DEFAULT OBG_HH_BUCKETS
+#else
+#define OBG_HH_BUCKETS_DEFAULT 1
+#endif
 constexpr uint32_t HH_LOG = 14, HH_SLOTS = 1u << HH_LOG, HH_EMPTY = 0xFFFFFFFFu;
 constexpr int HH_PROBES = 6;
-constexpr uint32_t HH_GIVE_UP = 4096;
+constexpr uint32_t HH_GIVE_UP = OBG_HH_BUCKETS_DEFAULT ? 32768 : 4096;   // full buckets spill a steady trickle (Poisson tail)
 
-// one add of `cnt` to leaf `idx` (cube order); returns false if the table had no room
+// One add of `cnt` to leaf `idx` (cube order); returns false if the table had
+// no room.  The table is 2^12 buckets of four (key, count) slots: a lookup is
+// ONE 16-byte read of the bucket's keys and four compares, so a warp does not
+// iterate to the longest probe sequence of its 32 lanes (linear probing over
+// single slots cost ~2.7 rounds per pixel run at a 25 % load factor: 50 warp
+// instructions per pixel slot, profiles/r02_ncu_hist6_c3.md).  A new key takes
+// the first empty slot of its bucket (atomicCAS, slots in order, so a key
+// never lands twice); a full bucket sends the add to global memory.
+#ifndef OBG_HH_BUCKETS
+#define OBG_HH_BUCKETS 1
+#endif
 __device__ __forceinline__ bool hh_add(uint32_t* keys, uint32_t* cnts, uint32_t idx, uint32_t cnt) {
+#if OBG_HH_BUCKETS
+  const uint32_t b4 = ((idx * 0x9E3779B1u) >> (32 - (HH_LOG - 2))) * 4u;
+  const uint4 k = *reinterpret_cast<const uint4*>(keys + b4);
+  int slot = k.x == idx ? 0 : k.y == idx ? 1 : k.z == idx ? 2 : k.w == idx ? 3 : -1;
+  if (slot < 0) {
+#pragma unroll 1
+    for (int t = 0; t < 4 && slot < 0; ++t) {
+      uint32_t cur = *reinterpret_cast<volatile uint32_t*>(keys + b4 + t);
+      if (cur == HH_EMPTY) {
+        cur = atomicCAS(keys + b4 + t, HH_EMPTY, idx);               // the old key: EMPTY = claimed
+        if (cur == HH_EMPTY) cur = idx;
+      }
+      if (cur == idx) slot = t;
+    }
+    if (slot < 0) return false;
+  }
+  atomicAdd(cnts + b4 + slot, cnt);
+  return true;
+#else
   uint32_t h = (idx * 0x9E3779B1u) >> (32 - HH_LOG);
 #pragma unroll 1
   for (int p = 0; p < HH_PROBES; ++p) {
@@ -3965,6 +3999,7 @@ __device__ __forceinline__ bool hh_add(uint32_t* keys, uint32_t* cnts, uint32_t 
     h = (h + 1u) & (HH_SLOTS - 1u);
   }
   return false;
+#endif
 }
 
 template <int L>
