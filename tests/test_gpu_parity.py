@@ -753,3 +753,45 @@ def test_l7_full_cell_models(cuda, n_cells, drop):
     # bit-packed output takes the same path
     packed = obg.classify(model, torch.from_numpy(probe).cuda(), packed=True).cpu().numpy()
     assert np.array_equal(np.unpackbits(packed, axis=1, bitorder="little")[:, :h * w].reshape(3, h, w).astype(bool), got)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("level", ["0", "1", "2"])
+def test_dependent_launch_levels(cuda, level):
+    """OBG_PDL = 0 / 1 / 2 (no programmatic dependent launches / the merge /
+    also a classify flagged after_build): the same model and masks, eagerly and
+    as a captured step.  The level is read once per process, hence a child."""
+    import subprocess
+    import sys
+    import textwrap
+    code = textwrap.dedent('''
+        import hashlib, numpy as np, torch
+        import paper_1412_1945_b200 as obg
+        from paper_1412_1945_b200.pipeline import CapturedStep
+        rng = np.random.default_rng(5)
+        base = rng.integers(0, 256, size=(1, 1, 1, 3))
+        train = torch.from_numpy(np.clip(base + rng.integers(-30, 31, size=(12, 96, 128, 3)), 0, 255).astype(np.uint8)).cuda()
+        test = torch.from_numpy(np.clip(base + rng.integers(-60, 61, size=(5, 96, 128, 3)), 0, 255).astype(np.uint8)).cuda()
+        h = hashlib.sha256()
+        for L in (4, 5, 6):
+            cfg = obg.ModelConfig(levels=L, threshold=0.5, training_frames=12)
+            m = obg.build_background_model_device(train, cfg)
+            masks = obg.classify(m, test, after_build=True)
+            step = CapturedStep(train, test, cfg)
+            for _ in range(3):
+                out = step.step()
+            torch.cuda.synchronize()
+            assert torch.equal(out, masks)
+            assert step.model.trees[0][0].to_bytes() == m.trees[0][0].to_bytes()
+            h.update(m.trees[0][0].to_bytes()); h.update(masks.cpu().numpy().tobytes())
+        print("DIGEST", h.hexdigest())
+    ''')
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for lv in sorted({"0", level}):
+        env = dict(os.environ, OBG_PDL=lv, PYTHONPATH=root + os.pathsep + os.environ.get("PYTHONPATH", ""))
+        res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+        assert res.returncode == 0, res.stderr[-2000:]
+        outs[lv] = [ln for ln in res.stdout.splitlines() if ln.startswith("DIGEST")][0]
+    assert outs[level] == outs["0"]
