@@ -925,6 +925,9 @@ __device__ __forceinline__ void flush_segment(uint32_t* s_bits, uint32_t* dst, i
 #ifndef OBG_ALIGN_TREES
 #define OBG_ALIGN_TREES 1
 #endif
+#ifndef OBG_BUILD_STAGES3
+#define OBG_BUILD_STAGES3 1         // 0: two register buffers at every depth (A/B)
+#endif
 #ifndef OBG_BUILD_NOLOOKUP
 #define OBG_BUILD_NOLOOKUP 0      // experiment: stream the frames without lookups (load-structure bound)
 #endif
@@ -991,14 +994,33 @@ k_build_flat(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_
       fp += STEP;                                                                              \
       ++k;                                                                                     \
     }
-    constexpr int STAGES = 2;
-    uint32_t wa[12], wb[12];
+    // L = 6: three register buffers, two units in flight per thread while the
+    // third is looked up.  ncu's source page puts 28 % of K1's stall samples on
+    // the first use of a freshly loaded unit (profiles/r02_ncu_build_hot_lines.md);
+    // the third buffer costs spills only outside the steady-state loop.  A/B
+    // (profiles/ab_r02/r02_ab_stages3.txt): C3 model 80.5 -> 79.6 us, C4
+    // constant L6 134.7 -> 131.7 us; L = 4 / 5 measured +-1 % and keep two.
+    constexpr int STAGES = (L == 6 && OBG_BUILD_STAGES3) ? 3 : 2;
     uint32_t sink = 0;
-    if (0 < n_lane) load_unit_at(fp, wa);
-    for (int32_t k = 0; k < n_it;) {
-      OBG_BUILD_STEP(wa, wb)
-      if (k >= n_it) break;
-      OBG_BUILD_STEP(wb, wa)
+    if constexpr (STAGES == 3) {
+      uint32_t wa[12], wb[12], wc[12];
+      if (0 < n_lane) load_unit_at(fp, wa);
+      if (1 < n_lane) load_unit_at(fp + STEP, wb);
+      for (int32_t k = 0; k < n_it;) {
+        OBG_BUILD_STEP(wa, wc)
+        if (k >= n_it) break;
+        OBG_BUILD_STEP(wb, wa)
+        if (k >= n_it) break;
+        OBG_BUILD_STEP(wc, wb)
+      }
+    } else {
+      uint32_t wa[12], wb[12];
+      if (0 < n_lane) load_unit_at(fp, wa);
+      for (int32_t k = 0; k < n_it;) {
+        OBG_BUILD_STEP(wa, wb)
+        if (k >= n_it) break;
+        OBG_BUILD_STEP(wb, wa)
+      }
     }
 #undef OBG_BUILD_STEP
     if (OBG_BUILD_NOLOOKUP && sink == 0x9E3779B9u) ws[0] = sink;     // keep the loads (experiment only)
