@@ -1760,9 +1760,15 @@ __device__ __forceinline__ void l7c_pair(const uint32_t (&w)[12], uint32_t k7, u
   far_b = (P >> 16) >= L7C_N;
 }
 
+// `blind` (warp-uniform): set every pixel's bit without looking it up first.
+// Check-before-set pays when most pixels hit; on frames whose pixels mostly
+// miss (uniform-random 4K frames at L = 7: 2 M leaves, ~60 % first sightings
+// per CTA segment) every group takes both the lookups and the atomics, 44
+// instructions per pixel; the blind form is ~13.  The kernel switches per warp
+// on the miss count of the last checked unit (`nmiss`, see k_build_l7c).
 template <int K>
 __device__ __forceinline__ void build_pairs_l7c(const uint32_t (&w)[12], bool valid, uint32_t k7,
-                                                uint32_t* __restrict__ gcube) {
+                                                uint32_t* __restrict__ gcube, bool blind, uint32_t& nmiss) {
   uint32_t ad[4], bs[4], fr[4], v[4], go[4];
   {
     uint32_t rq0, q0, rq1, q1;
@@ -1772,6 +1778,17 @@ __device__ __forceinline__ void build_pairs_l7c(const uint32_t (&w)[12], bool va
     go[1] = ((rq0 >> 16) << 11) | ((q0 >> 16) << 2);
     go[2] = ((rq1 & 0x7Fu) << 11) | ((q1 & 0xFFFFu) << 2);
     go[3] = ((rq1 >> 16) << 11) | ((q1 >> 16) << 2);
+  }
+  if (blind) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (valid) {
+        const uint32_t bit = 1u << (bs[j] & 31u);
+        if (!fr[j]) reds_or_at(ad[j], bit);
+        else atomicOr(reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(gcube) + go[j]), bit);
+      }
+    }
+    return;
   }
   if (!__any_sync(0xFFFFFFFFu, (fr[0] | fr[1] | fr[2] | fr[3]) != 0u)) {
     // no pixel of the warp's 4-pixel group in the global window (the common
@@ -1796,6 +1813,7 @@ __device__ __forceinline__ void build_pairs_l7c(const uint32_t (&w)[12], bool va
     for (int j = 0; j < 4; ++j) {
       if (valid && !(v[j] & 1u)) {
         const uint32_t bit = 1u << (bs[j] & 31u);
+        ++nmiss;
         if (!fr[j]) reds_or_at(ad[j], bit);
         else atomicOr(reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(gcube) + go[j]), bit);
       }
@@ -1803,12 +1821,36 @@ __device__ __forceinline__ void build_pairs_l7c(const uint32_t (&w)[12], bool va
   }
 }
 
+// Per-warp mode of the one-pass L7 build: a checked unit counts its missed
+// pixels; above L7C_BLIND_MISSES of the warp's 512 the next L7C_BLIND_RUN units
+// go blind, then one checked unit measures again.
+#ifndef OBG_L7_BLIND
+#define OBG_L7_BLIND 1
+#endif
+constexpr uint32_t L7C_BLIND_MISSES = 160;       // ~31 % of a warp-unit's pixels
+constexpr int L7C_BLIND_RUN = 16;
+struct L7Mode {
+  int blind_left = 0;
+};
 __device__ __forceinline__ void build_unit_l7c(const uint32_t (&w)[12], bool valid, uint32_t k7,
-                                               uint32_t* __restrict__ gcube) {
-  build_pairs_l7c<0>(w, valid, k7, gcube);
-  build_pairs_l7c<2>(w, valid, k7, gcube);
-  build_pairs_l7c<4>(w, valid, k7, gcube);
-  build_pairs_l7c<6>(w, valid, k7, gcube);
+                                               uint32_t* __restrict__ gcube, L7Mode& mode) {
+  uint32_t nmiss = 0;
+  if (OBG_L7_BLIND && mode.blind_left > 0) {                     // warp-uniform
+    build_pairs_l7c<0>(w, valid, k7, gcube, true, nmiss);
+    build_pairs_l7c<2>(w, valid, k7, gcube, true, nmiss);
+    build_pairs_l7c<4>(w, valid, k7, gcube, true, nmiss);
+    build_pairs_l7c<6>(w, valid, k7, gcube, true, nmiss);
+    --mode.blind_left;
+    return;
+  }
+  build_pairs_l7c<0>(w, valid, k7, gcube, false, nmiss);
+  build_pairs_l7c<2>(w, valid, k7, gcube, false, nmiss);
+  build_pairs_l7c<4>(w, valid, k7, gcube, false, nmiss);
+  build_pairs_l7c<6>(w, valid, k7, gcube, false, nmiss);
+  // a lane with 5+ missed pixels of its 16 stands for a warp-unit above ~30 %
+  // (misses spread evenly over the lanes of uniform-random frames; a natural
+  // scene's few first sightings stay below)
+  if (OBG_L7_BLIND && __any_sync(0xFFFFFFFFu, nmiss >= 8u)) mode.blind_left = L7C_BLIND_RUN;
 }
 
 __global__ void __launch_bounds__(L7C_BLOCK, 1)
@@ -1844,14 +1886,15 @@ k_build_l7c(const uint8_t* __restrict__ frames, int64_t units_per_frame, int64_t
     constexpr int64_t STEP = 48 * int64_t(L7C_BLOCK);
     const uint8_t* fp = frames + 48 * (u + rel0 + lane);
     uint32_t wa[12], wb[12];
+    L7Mode mode;                                                  // a fresh segment starts checked
     if (0 < n_lane) load_unit_at(fp, wa);
     for (int32_t k = 0; k < n_it;) {
       if (k + 1 < n_lane) load_unit_at(fp + STEP, wb);
-      build_unit_l7c(wa, k < n_lane, k7, dst);
+      build_unit_l7c(wa, k < n_lane, k7, dst, mode);
       fp += STEP;
       if (++k >= n_it) break;
       if (k + 1 < n_lane) load_unit_at(fp + STEP, wa);
-      build_unit_l7c(wb, k < n_lane, k7, dst);
+      build_unit_l7c(wb, k < n_lane, k7, dst, mode);
       fp += STEP;
       ++k;
     }
