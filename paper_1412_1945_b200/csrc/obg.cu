@@ -1828,7 +1828,13 @@ __device__ __forceinline__ void build_pairs_l7c(const uint32_t (&w)[12], bool va
 #define OBG_L7_BLIND 1
 #endif
 constexpr uint32_t L7C_BLIND_MISSES = 160;       // ~31 % of a warp-unit's pixels
-constexpr int L7C_BLIND_RUN = 16;
+#ifndef OBG_L7_BLIND_RUN
+#define OBG_L7_BLIND_RUN 16
+#endif
+#ifndef OBG_L7_BLIND_THR
+#define OBG_L7_BLIND_THR 8
+#endif
+constexpr int L7C_BLIND_RUN = OBG_L7_BLIND_RUN;
 struct L7Mode {
   int blind_left = 0;
 };
@@ -1850,7 +1856,7 @@ __device__ __forceinline__ void build_unit_l7c(const uint32_t (&w)[12], bool val
   // a lane with 5+ missed pixels of its 16 stands for a warp-unit above ~30 %
   // (misses spread evenly over the lanes of uniform-random frames; a natural
   // scene's few first sightings stay below)
-  if (OBG_L7_BLIND && __any_sync(0xFFFFFFFFu, nmiss >= 8u)) mode.blind_left = L7C_BLIND_RUN;
+  if (OBG_L7_BLIND && __any_sync(0xFFFFFFFFu, nmiss >= uint32_t(OBG_L7_BLIND_THR))) mode.blind_left = L7C_BLIND_RUN;
 }
 
 __global__ void __launch_bounds__(L7C_BLOCK, 1)
