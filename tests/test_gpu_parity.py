@@ -705,6 +705,10 @@ def test_detect_host_many_frames_cross_staging_passes(cuda):
     model = obg.build_background_model(list(train), cfg)
     want = obg.classify(model, torch.from_numpy(probe).cuda()).cpu().numpy().astype(bool)
     assert np.array_equal(obg.detect_octree_batch(model, probe), want)
+    # the calling thread's staging buffers can be released and are rebuilt on demand
+    _lib.load().obg_host_stage_release()
+    assert np.array_equal(obg.detect_octree(model, probe[3]), want[3])
+    _lib.load().obg_host_stage_release()
 
 
 @pytest.mark.gpu
