@@ -4968,7 +4968,8 @@ int obg_detect_host(const uint8_t* frames, int n_frames, int height, int width, 
     const uint8_t* src = frames + f0 * 3 * P;
     uint8_t* dst = mask + f0 * P;
     // in: two halves (cut at a multiple of 256 bytes), stage -> H2D
-    const int64_t cut_in = (in_bytes / 2) & ~int64_t(255);
+    // (frames below 1 MiB go as one piece: the second copy call would cost more than the overlap)
+    const int64_t cut_in = in_bytes >= (int64_t(1) << 20) ? (in_bytes / 2) & ~int64_t(255) : 0;
     const int64_t in_off[3] = {0, cut_in, in_bytes};
     for (int h = 0; h < 2; ++h) {
       const int64_t len = in_off[h + 1] - in_off[h];
@@ -4982,7 +4983,7 @@ int obg_detect_host(const uint8_t* frames, int n_frames, int height, int width, 
                                            s.dev_out, nullptr, st))
       return rc;
     // out: two halves, D2H -> copy out (the second transfer overlaps the first copy)
-    const int64_t cut_out = (out_bytes / 2) & ~int64_t(255);
+    const int64_t cut_out = out_bytes >= (int64_t(1) << 20) ? (out_bytes / 2) & ~int64_t(255) : 0;
     const int64_t out_off[3] = {0, cut_out, out_bytes};
     for (int h = 0; h < 2; ++h) {
       const int64_t len = out_off[h + 1] - out_off[h];

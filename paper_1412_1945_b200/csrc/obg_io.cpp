@@ -378,6 +378,13 @@ static int pool_copy_blocks(const uint8_t* const* srcs, int n, int64_t bytes_eac
   for (int i = 0; i < n; ++i)
     if (!srcs[i]) return obg_set_error(OBG_EINVAL, "null source %d", i);
   constexpr int64_t CHUNK = int64_t(1) << 18;                 // 256 KiB pieces spread over the pool
+  if (bytes_each * n <= CHUNK) {                              // small: waking the pool costs more than the copy
+    for (int i = 0; i < n; ++i) {
+      if (streaming) copy_streaming(dst + i * bytes_each, srcs[i], size_t(bytes_each));
+      else memcpy(dst + i * bytes_each, srcs[i], size_t(bytes_each));
+    }
+    return OBG_OK;
+  }
   const int64_t per = (bytes_each + CHUNK - 1) / CHUNK;
   const int64_t tasks = per * n;
   if (tasks > (int64_t(1) << 30)) return obg_set_error(OBG_EUNSUPPORTED, "copy too large");
